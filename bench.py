@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: teams-distribute-parallel-for fp64 sum reduction, N = 2^30 per GPU.
+
+BASELINE.json metric "reduction GB/s (frac of HBM peak) at N=2^30, 1/2/4/8
+B200 vs CPU ref" on configs[1] ("teams distribute parallel for fp64 sum
+reduction, N=2^30, SPMD mode, 1 B200").  One step = one pass of the hot path
+over the resident 8 GiB fp64 array: omprt_reduce (schedule distribute,
+SPMD, last-team-finishes) and, for N > 1 GPUs, the one NCCL all-reduce of the
+per-GPU partial plus the ordered combine.  Weak scaling: every rank owns a
+2^30-element shard (static_bounds over ranks of a G*2^30 global space).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU restatement
+of the reference's own host-fallback algorithm (oracle/, "port") on this
+host's cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "reduction GB/s (frac of HBM peak) at N=2^30, 1/2/4/8 B200 vs CPU ref"
+N_PER_GPU = 1 << 30
+ELEM = 8  # fp64
+SEED = 0x210603219
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=1000)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--teams", type=int, default=0, help="0: 2 teams per SM")
+    p.add_argument("--threads", type=int, default=1024)
+    p.add_argument("--sched", default="distribute")
+    p.add_argument("--unroll", type=int, default=0)
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU")
+    return p.parse_args()
+
+
+def peaks() -> dict:
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic():
+    """dram read+write bytes per launch of the reduce kernel from the committed
+    ncu --set full capture (profiles/), or None."""
+    f = ROOT / "profiles" / "ncu_reduce_f64.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text()).get("dram_bytes_per_launch")
+        except ValueError:
+            return None
+    return None
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML while running."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples: list[tuple[float, int]] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((time.perf_counter(), mhz))
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def start(self):
+        if self.nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+        mhz = [m for _, m in self.samples]
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(mhz)}
+
+
+# --------------------------------------------------------------------- CPU arm
+
+def cpu_reference(n_sample: int, steps: int, warmup: int, teams: int, threads: int,
+                  min_seconds: float = 0.0) -> dict:
+    """The reference's CPU path, restated in C (oracle/, kind "port"): the
+    host fallback's algorithm (host.py:567-582) — every OpenMP thread folds its
+    for_static_init block in order, partials combined in global-id order —
+    parallelised over the forge threads on all host cores, over an in-memory
+    fp64 array of n_sample elements."""
+    from oracle import oracle as O
+
+    x = O.fill(n_sample, O.F64, SEED, 0)
+    for _ in range(warmup):
+        O.reduce(x, 0, n_sample - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, teams, threads)
+    t0 = time.perf_counter()
+    done = 0
+    while done < steps or (time.perf_counter() - t0) < min_seconds:
+        O.reduce(x, 0, n_sample - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, teams, threads)
+        done += 1
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "steps": done, "gbs": n_sample * ELEM * done / dt / 1e9,
+            "cores": O.num_threads(), "n": n_sample}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_sample = 1 << 25
+    teams = args.teams or 296
+    r = cpu_reference(n_sample, args.steps, args.warmup, teams, args.threads)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(r["gbs"], 3),
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": r["steps"],
+        "warmup": args.warmup,
+        "ms_per_step": round(r["seconds"] / r["steps"] * 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (splitmix64 counter-based fp64 in [0,1))",
+        "config": {"workload": "C2 teams distribute parallel for fp64 sum reduction",
+                   "n_per_step": n_sample, "teams": teams, "threads": args.threads,
+                   "schedule": "distribute"},
+        "cpu_baseline": {"value": round(r["gbs"], 3), "unit": "GB/s", "cores": r["cores"],
+                         "kind": "port",
+                         "sample": f"{n_sample} fp64 elements (256 MiB) per step, host fallback "
+                                   f"order (host.py:567-582) over {teams}x{args.threads} "
+                                   "OpenMP threads, parallel over host cores"},
+        "e2e": {"value": round(r["gbs"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU arm
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2106_03219_b200 import _lib, offload, parallel, runtime
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.ensure_device(local)
+    if args.unroll:
+        runtime.set_unroll(args.unroll)
+
+    n = args.n
+    G = world
+    glb, gub = 0, G * n - 1
+    lo, hi = parallel.shard(glb, gub, rank, G)
+    nloc = hi - lo + 1
+    sms = runtime.num_sms()
+    teams = args.teams or 2 * sms
+    threads = args.threads
+    x = runtime.synthetic(nloc, "f64", SEED, 0, offset=lo, device=dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    partial = torch.zeros(1, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        partial.zero_()
+        runtime.reduce(x, "add", sched=args.sched, teams=teams, threads=threads, out=partial)
+        if G > 1:
+            parallel.allreduce_partial(partial, "add")
+        runtime.combine_partials(partial, "add", out=out)
+
+    step()
+    torch.cuda.synchronize()
+    got = float(partial.item())
+
+    for _ in range(args.warmup):
+        step()
+    # kernel-only timing (CUDA events on the launching stream)
+    k_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(min(args.steps, 200))]
+    for a, b in k_ev:
+        a.record(stream)
+        runtime.reduce(x, "add", sched=args.sched, teams=teams, threads=threads, out=partial)
+        b.record(stream)
+    torch.cuda.synchronize()
+    k_ms = [a.elapsed_time(b) for a, b in k_ev]
+    k_avg_ms = sum(k_ms) / len(k_ms)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.1)
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_bytes = G * n * ELEM
+    gbs = total_bytes * args.steps / (ms_max / 1e3) / 1e9
+
+    # end to end through the C-ABI host-buffer call (pinned host -> HBM each step)
+    e2e = None
+    if args.e2e_steps > 0:
+        hx = torch.empty(nloc, dtype=torch.float64, pin_memory=True)
+        hx.copy_(x)
+        cell = torch.zeros(1, dtype=torch.float64)
+        offload.reduce_host(hx, cell, op="add", sched=args.sched, teams=teams, threads=threads)
+        got_e2e = float(cell.item())
+        if G > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            cell.zero_()
+            offload.reduce_host(hx, cell, op="add", sched=args.sched, teams=teams,
+                                threads=threads)
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        if G > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(total_bytes * args.e2e_steps / float(te.item()) / 1e9, 3),
+               "unit": "GB/s", "h2d_bytes_per_step": nloc * ELEM + ELEM,
+               "d2h_bytes_per_step": ELEM,
+               "path": "omprt_reduce_host (C ABI, pinned host buffer, copy-in + reduce + "
+                       "copy-out per step)"}
+        del hx
+    cpu = None
+    parity = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        # the CPU-baseline leg: the oracle is the checker of the device result
+        # (exact sum of the generated data) and the timed CPU reference path
+        from oracle import oracle as O
+
+        exact = O.exact_sum_gen(glb, gub, O.F64, seed=SEED)
+        parity = {"rel_err_vs_exact": abs(got - exact) / exact, "tolerance": 1e-6}
+        if e2e is not None:
+            parity["e2e_rel_err_vs_exact"] = abs(got_e2e - exact) / exact
+        if parity["rel_err_vs_exact"] > 1e-6:
+            raise SystemExit(f"parity failure: {got} vs exact {exact}")
+        r = cpu_reference(1 << 26, 3, 1, teams, threads, min_seconds=10.0)
+        cpu = {"value": round(r["gbs"], 3), "unit": "GB/s", "cores": r["cores"], "kind": "port",
+               "sample": f"{r['n']} fp64 elements (512 MiB, in host memory) x {r['steps']} "
+                         f"passes ({r['seconds']:.1f} s), host fallback order "
+                         f"(host.py:567-582) over {teams}x{threads} OpenMP threads"}
+    if rank == 0:
+        pk = peaks()
+        achieved = n * ELEM / (k_avg_ms / 1e3) / 1e9
+        traffic = ncu_traffic()
+        line = {
+            "metric": METRIC,
+            "value": round(gbs, 3),
+            "unit": "GB/s",
+            "n_gpus": G,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 5),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (splitmix64 counter-based fp64 in [0,1), generated on device)",
+            "config": {"workload": "C2 teams distribute parallel for fp64 sum reduction, SPMD",
+                       "n_per_gpu": n, "n_global": G * n, "schedule": args.sched,
+                       "teams": teams, "threads": threads, "mode": "spmd",
+                       "parallelism": f"dp{G} (static_bounds shards + NCCL all-reduce)",
+                       "l2": "input 8 GiB per GPU >> 126 MB L2; no flush needed",
+                       "frac_of_hbm_peak": round(gbs / G / pk["hbm_gbs"], 4),
+                       "frac_of_nominal_8tbs": round(gbs / G / 8000.0, 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2),
+                         "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(achieved / pk["hbm_gbs"], 4),
+                         "traffic": traffic,
+                         "peak_source": pk["source"],
+                         "kernel": "omprt::k_reduce<double,ADD>",
+                         "kernel_avg_ms": round(k_avg_ms, 5),
+                         "algorithmic_bytes_per_launch": n * ELEM},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * 2,
+            "clocks": clocks,
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,310 @@
+// generic.cuh — the team-shared smart stack (__kmpc_alloc_shared /
+// __kmpc_free_shared), generic-mode execution on named barriers, and the
+// scoped-atomic probe.
+//
+// Reference: runtime.mc:67-91 (arena), devicert.Arena devicert.py:124-148
+// (semantics and trap codes 1/2/3), vgpu.py:171-250 (team-shared layout,
+// poison 0xAA for loader_uninitialized), runtime.mc:136-186 (atomics).
+#pragma once
+
+#include <cuda/atomic>
+
+#include "kernels.cuh"
+
+namespace omprt {
+
+// ------------------------------------------------------------------ arena
+//
+// Offsets are byte offsets, as the reference returns (runtime.mc:73-84).
+// [0, capacity) lives in this team's shared memory.  With heap_fallback the
+// arena continues into a per-team slice of global memory: offsets
+// >= capacity address heap byte (off - capacity).  Once an allocation spills,
+// later allocations also go to the heap until the heap stack empties again,
+// so the whole arena stays one LIFO stack and non-LIFO frees still trap.
+struct ArenaState {
+  uint64_t cursor;       // __arena_cursor (runtime.mc:67-68), zero-initialised per team
+  uint64_t heap_cursor;  // bytes live in the heap part
+  uint64_t capacity;     // shared-memory capacity (ARENA_CAPACITY by default)
+  uint64_t heap_cap;     // heap bytes available to this team
+  unsigned char *smem;
+  unsigned char *heap;
+  int heap_fallback;
+};
+
+OMPRT_D uint64_t arena_align(uint64_t b) {
+  return (b + OMPRT_ARENA_ALIGN - 1) / OMPRT_ARENA_ALIGN * OMPRT_ARENA_ALIGN;
+}
+
+// Returns the offset, or -code (1 overflow, 3 not thread 0) — the caller
+// turns a negative result into a trap.
+OMPRT_D int64_t kmpc_alloc_shared(ArenaState &a, uint64_t bytes, uint32_t caller_tid) {
+  if (caller_tid != 0) return -OMPRT_TRAP_NON_UNIFORM_ALLOC;
+  const uint64_t need = arena_align(bytes);
+  if (a.heap_cursor == 0) {
+    if (bytes <= a.capacity && a.cursor + need <= a.capacity) {
+      const uint64_t off = a.cursor;
+      a.cursor += need;
+      return (int64_t)off;
+    }
+    if (!a.heap_fallback) return -OMPRT_TRAP_SHARED_OVERFLOW;
+  }
+  if (need > a.heap_cap - a.heap_cursor) return -OMPRT_TRAP_SHARED_OVERFLOW;
+  const uint64_t off = a.capacity + a.heap_cursor;
+  a.heap_cursor += need;
+  return (int64_t)off;
+}
+
+// Returns 0 or -code (2 non-LIFO, 3 not thread 0).
+OMPRT_D int64_t kmpc_free_shared(ArenaState &a, uint64_t off, uint64_t bytes,
+                                 uint32_t caller_tid) {
+  if (caller_tid != 0) return -OMPRT_TRAP_NON_UNIFORM_ALLOC;
+  const uint64_t need = arena_align(bytes);
+  if (a.heap_fallback && off >= a.capacity) {
+    if (off + need - a.capacity != a.heap_cursor) return -OMPRT_TRAP_NON_LIFO_FREE;
+    a.heap_cursor = off - a.capacity;
+    return 0;
+  }
+  if (a.heap_cursor != 0) return -OMPRT_TRAP_NON_LIFO_FREE;
+  if (off + need != a.cursor) return -OMPRT_TRAP_NON_LIFO_FREE;
+  a.cursor = off;
+  return 0;
+}
+
+OMPRT_D unsigned char *arena_ptr(const ArenaState &a, uint64_t off) {
+  return off < a.capacity ? a.smem + off : a.heap + (off - a.capacity);
+}
+
+struct ArenaCfg {
+  int64_t capacity;
+  int64_t heap_per_team;
+  unsigned char *heap;  // teams * heap_per_team bytes (may be null without fallback)
+  int heap_fallback;
+};
+
+OMPRT_D void arena_init(ArenaState &a, const ArenaCfg &c, unsigned char *smem) {
+  a.cursor = 0;
+  a.heap_cursor = 0;
+  a.capacity = (uint64_t)c.capacity;
+  a.heap_cap = c.heap_fallback ? (uint64_t)c.heap_per_team : 0;
+  a.smem = smem;
+  a.heap = c.heap_fallback ? c.heap + (int64_t)blockIdx.x * c.heap_per_team : nullptr;
+  a.heap_fallback = c.heap_fallback;
+}
+
+// Replay an alloc/free script (devicert.Arena parity; test_devicert.py:114-208).
+// Results per op: offset (alloc), 0 (free), -code at the trapping op and
+// kArenaSkipped after it.
+constexpr int64_t kArenaSkipped = -0x7fff;
+
+__global__ void k_arena_replay(const int64_t *__restrict__ script, int nops, int caller_tid,
+                               ArenaCfg cfg, int64_t *__restrict__ results) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ ArenaState st;
+  __shared__ int64_t s_res;
+  // loader_uninitialized poison (vgpu.py:64-77 POISON_BYTE 0xAA)
+  for (int64_t i = threadIdx.x; i < cfg.capacity; i += blockDim.x) dsm[i] = 0xAA;
+  if (threadIdx.x == 0) arena_init(st, cfg, dsm);
+  __syncthreads();
+  int64_t *res = results + (int64_t)blockIdx.x * nops;
+  for (int op = 0; op < nops; ++op) {
+    const int64_t kind = script[3 * op], bytes = script[3 * op + 1], foff = script[3 * op + 2];
+    if (threadIdx.x == (uint32_t)caller_tid) {
+      // the calling thread runs the runtime routine with its own thread id
+      s_res = (kind == OMPRT_ARENA_ALLOC)
+                  ? kmpc_alloc_shared(st, (uint64_t)bytes, threadIdx.x)
+                  : kmpc_free_shared(st, (uint64_t)foff, (uint64_t)bytes, threadIdx.x);
+      if (s_res < 0) raise_trap((int)-s_res, (int)-s_res);
+    }
+    __syncthreads();
+    const int64_t r = s_res;
+    if (threadIdx.x == 0) res[op] = r;
+    if (r < 0) {
+      if (threadIdx.x == 0)
+        for (int k = op + 1; k < nops; ++k) res[k] = kArenaSkipped;
+      return;
+    }
+    if (kind == OMPRT_ARENA_ALLOC && bytes > 0) {
+      // data path: the whole team writes a tag through the returned offset,
+      // then reads it back with a different thread->byte mapping
+      unsigned char *p = arena_ptr(st, (uint64_t)r);
+      const unsigned tag = (unsigned)(blockIdx.x * 131u + op * 17u);
+      for (int64_t j = threadIdx.x; j < bytes; j += blockDim.x)
+        p[j] = (unsigned char)((tag + (unsigned)j) & 0xffu);
+      __syncthreads();
+      for (int64_t j = (int64_t)blockDim.x - 1 - threadIdx.x; j < bytes; j += blockDim.x)
+        if (j >= 0 && p[j] != (unsigned char)((tag + (unsigned)j) & 0xffu))
+          raise_trap(OMPRT_TRAP_ABORT, 0);
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------ generic mode
+//
+// One CTA = one team = 1 main warp + P/32 worker warps.  Named barriers:
+//   1  fork       main warp + all workers (bar.sync)
+//   2  in-region  workers only            (the parallel region's barrier)
+//   3  join       workers bar.arrive, main warp bar.sync
+// Lane 0 of the main warp is the team's initial thread (omp thread 0 in the
+// sequential part): it owns the arena (tid-0 contract, runtime.mc:76, 87).
+enum : int { kWorkExit = 0, kWorkRegion = 1 };
+
+constexpr uint32_t kBarFork = 1, kBarRegion = 2, kBarJoin = 3;
+
+template <class T, int OP, int U>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_generic(const T *__restrict__ x, int64_t lb, int64_t ub, int P, int ordered, int64_t pad,
+              ArenaCfg cfg, Workspace ws, T *out, int64_t *team_offsets) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ ArenaState st;
+  __shared__ volatile int s_work;
+  __shared__ int64_t s_tlb, s_tub;
+  __shared__ uint64_t s_off;
+  const uint32_t nall = 32u + (uint32_t)P;
+  const uint32_t lane = lane_id();
+
+  if (warp_id() == 0) {
+    // ------------------------------------------------ main warp (sequential part)
+    T team_val = Red<OP, T>::identity();
+    if (lane == 0) {
+      arena_init(st, cfg, dsm);
+      const Bounds tb = team_block(lb, ub, blockIdx.x, gridDim.x);  // distribute
+      s_tlb = tb.lower;
+      s_tub = tb.upper;
+      // an optional earlier allocation (pad) and then the globalised
+      // `parts[P]` + the team reduction variable, stacked LIFO
+      int64_t r = 0;
+      if (pad > 0) r = kmpc_alloc_shared(st, (uint64_t)pad, 0);
+      if (r >= 0) r = kmpc_alloc_shared(st, (uint64_t)(P + 1) * sizeof(T), 0);
+      if (r < 0) {
+        raise_trap((int)-r, (int)-r);
+        s_work = kWorkExit;
+      } else {
+        s_off = (uint64_t)r;
+        s_work = kWorkRegion;
+        if (team_offsets) team_offsets[blockIdx.x] = r;
+      }
+    }
+    __syncwarp();
+    named_barrier_sync(kBarFork, nall);  // fork (or release to exit on trap)
+    if (s_work == kWorkRegion) {
+      named_barrier_sync(kBarJoin, nall);  // join: wait for the workers
+      if (lane == 0) {
+        T *parts = (T *)arena_ptr(st, s_off);
+        T v = Red<OP, T>::identity();
+        if (ordered) {
+          for (int w = 0; w < P; ++w) v = Red<OP, T>::apply(v, parts[w]);
+        } else {
+          v = parts[P];
+        }
+        team_val = v;
+        int64_t r = kmpc_free_shared(st, s_off, (uint64_t)(P + 1) * sizeof(T), 0);
+        if (r == 0 && pad > 0) r = kmpc_free_shared(st, 0, (uint64_t)pad, 0);
+        if (r < 0) raise_trap((int)-r, (int)-r);
+        s_work = kWorkExit;
+      }
+      __syncwarp();
+      named_barrier_sync(kBarFork, nall);  // release the workers to exit
+    }
+    // -------------------------------------- teams reduction within the main warps
+    T *partials = (T *)ws.team_partials;
+    int last = 0;
+    if (lane == 0) {
+      partials[blockIdx.x] = team_val;
+      fence_acq_rel_gpu();
+      last = atomic_inc_acq_rel_gpu(ws.ticket, gridDim.x - 1) == gridDim.x - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      fence_acq_rel_gpu();
+      if (ordered) {
+        if (lane == 0 && !trap_raised())
+          *out = fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x);
+      } else {
+        T v = Red<OP, T>::identity();
+        for (uint32_t i = lane; i < gridDim.x; i += 32) v = Red<OP, T>::apply(v, ld_cg(partials + i));
+        v = warp_reduce<OP, T>(v, 32);
+        if (lane == 0 && !trap_raised()) *out = Red<OP, T>::apply(*out, v);
+      }
+    }
+  } else {
+    // ------------------------------------------------ worker state machine
+    const uint32_t wt = threadIdx.x - 32;  // omp thread id inside the parallel region
+    for (;;) {
+      named_barrier_sync(kBarFork, nall);
+      if (s_work == kWorkExit) break;
+      T *parts = (T *)arena_ptr(st, s_off);
+      const int64_t tlb = s_tlb, tub = s_tub;
+      if (ordered) {
+        // for_static_init over the team block, literal sequential chunk
+        int64_t mlb, mub;
+        static_bounds(tlb, tub, wt, P, mlb, mub);
+        T part = Red<OP, T>::identity();
+        for (int64_t i = mlb; i <= mub; ++i) part = Red<OP, T>::apply(part, x[i]);
+        parts[wt] = part;
+      } else {
+        ReduceBody<T, OP> body(x);
+        if (tub >= tlb) run_contiguous<U>(body, tlb, tub - tlb + 1, wt, (uint32_t)P);
+        // nested parallel reduce across the workers, scratch in the
+        // globalised arena block, synchronised on the workers-only barrier
+        const T v = warps_reduce_named<OP, T>(body.total(), (volatile T *)parts, 1, (uint32_t)P,
+                                              kBarRegion);
+        if (wt == 0) parts[P] = Red<OP, T>::apply(Red<OP, T>::identity(), v);
+      }
+      named_barrier_arrive(kBarJoin, nall);
+    }
+  }
+}
+
+// ------------------------------------------------------------ atomics probe
+//
+// seq_cst RMWs at device scope (the reference's constructs are seq_cst,
+// runtime.mc:131-134; IR atomic.<kind>.seq_cst.<ty>, selectors.py:40-46).
+template <class T> OMPRT_D T atomic_rmw(int kind, T *cell, T e, T d) {
+  cuda::atomic_ref<T, cuda::thread_scope_device> ref(*cell);
+  switch (kind) {
+    case OMPRT_ATOMIC_ADD:
+      return ref.fetch_add(e, cuda::std::memory_order_seq_cst);
+    case OMPRT_ATOMIC_MAX:
+      return ref.fetch_max(e, cuda::std::memory_order_seq_cst);
+    case OMPRT_ATOMIC_MIN:
+      return ref.fetch_min(e, cuda::std::memory_order_seq_cst);
+    case OMPRT_ATOMIC_XCHG:
+      return ref.exchange(e, cuda::std::memory_order_seq_cst);
+    case OMPRT_ATOMIC_CAS: {
+      T expected = e;
+      ref.compare_exchange_strong(expected, d, cuda::std::memory_order_seq_cst);
+      return expected;  // the observed value either way
+    }
+    default:  // INC: u32 only (validated on the host)
+      kmpc_flush();
+      return (T)atomic_inc_acq_rel_gpu((uint32_t *)cell, (uint32_t)e);
+  }
+}
+
+template <class T> OMPRT_D uint64_t as_word(T v) {
+  return (uint64_t)(typename std::make_unsigned<T>::type)v;
+}
+
+// Every thread of the grid applies one RMW to the single shared cell.
+template <class T>
+__global__ void k_atomic_probe(int kind, const uint64_t *__restrict__ ops,
+                               const uint64_t *__restrict__ desired, T *cell,
+                               uint64_t *__restrict__ old_out) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const T d = desired ? (T)desired[g] : T(0);
+  old_out[g] = as_word<T>(atomic_rmw<T>(kind, cell, (T)ops[g], d));
+}
+
+// Thread g applies one RMW to its own cell g (batched step_* semantics).
+template <class T>
+__global__ void k_atomic_apply(int kind, T *cells, const uint64_t *__restrict__ ops,
+                               const uint64_t *__restrict__ desired,
+                               uint64_t *__restrict__ old_out, int64_t n) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  const T d = desired ? (T)desired[g] : T(0);
+  old_out[g] = as_word<T>(atomic_rmw<T>(kind, cells + g, (T)ops[g], d));
+}
+
+}  // namespace omprt

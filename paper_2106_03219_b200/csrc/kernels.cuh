@@ -1,0 +1,386 @@
+// kernels.cuh — the `target teams distribute parallel for reduction` kernels.
+//
+//   k_reduce            SPMD: schedule -> coalesced team walk -> per-lane
+//                       accumulators -> warp shuffle + smem tree -> team
+//                       partial -> last-team-finishes ordered combine
+//   k_reduce_ordered    ORDERED: literal per-thread chunk loops, per-thread
+//                       partials combined in global thread order
+//   k_axpy_minmax       fused y = a*x + y (fmaf) with max/min of y
+//   k_dot               fp64 dot product
+//   k_bounds_dump       every thread's schedule_init result (parity)
+//   k_fill              counter-based synthetic data
+//   k_combine           ordered combine of per-rank partials
+#pragma once
+
+#include "loops.cuh"
+
+namespace omprt {
+
+constexpr int kMaxThreads = 1024;
+
+// Workspace layout (bytes): [0,256) ticket + pad | team partials | thread partials
+struct Workspace {
+  uint32_t *ticket;
+  unsigned char *team_partials;
+  unsigned char *thread_partials;
+};
+
+__host__ inline size_t ws_bytes(int teams, int threads, int mode, int slots) {
+  size_t b = 256 + (size_t)teams * 8 * slots;
+  b = (b + 255) & ~(size_t)255;
+  if (mode == OMPRT_MODE_ORDERED) b += (size_t)teams * threads * 8 * slots;
+  return b;
+}
+
+__host__ inline Workspace ws_carve(void *base, int teams, int slots) {
+  Workspace w;
+  unsigned char *p = (unsigned char *)base;
+  w.ticket = (uint32_t *)p;
+  w.team_partials = p + 256;
+  size_t off = 256 + (size_t)teams * 8 * slots;
+  off = (off + 255) & ~(size_t)255;
+  w.thread_partials = p + off;
+  return w;
+}
+
+// Last-team-finishes (__kmpc_nvptx_teams_reduce_nowait_v2 analog): thread 0
+// publishes the team value, takes a ticket with a device-scope acq_rel
+// atomic inc bounded by teams-1 (so the counter wraps back to 0 for the next
+// launch, step_inc devicert.py:105-107); the team holding the last ticket
+// combines every team partial in team-id order — deterministic regardless of
+// which team finished last.
+template <int OP, class T>
+OMPRT_D bool teams_ticket(T team_val, T *partials, uint32_t *ticket) {
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = team_val;
+    fence_acq_rel_gpu();
+    const uint32_t t = atomic_inc_acq_rel_gpu(ticket, gridDim.x - 1);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  const bool last = s_last != 0;
+  if (last) fence_acq_rel_gpu();
+  return last;
+}
+
+template <int OP, class T>
+OMPRT_D T combine_team_partials(const T *partials, T *scratch) {
+  T v = Red<OP, T>::identity();
+  for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x)
+    v = Red<OP, T>::apply(v, ld_cg(partials + i));
+  return block_reduce<OP, T>(v, scratch, blockDim.x);
+}
+
+// ------------------------------------------------------------------ bodies
+
+template <class T> OMPRT_D void unpack(const uint4 &r, T (&out)[16 / sizeof(T)]) {
+  static_assert(sizeof(uint4) == 16, "vector width");
+  union {
+    uint4 u;
+    T t[16 / sizeof(T)];
+  } cv;
+  cv.u = r;
+#pragma unroll
+  for (int j = 0; j < (int)(16 / sizeof(T)); ++j) out[j] = cv.t[j];
+}
+
+template <class T> OMPRT_D uint4 pack(const T (&in)[16 / sizeof(T)]) {
+  union {
+    uint4 u;
+    T t[16 / sizeof(T)];
+  } cv;
+#pragma unroll
+  for (int j = 0; j < (int)(16 / sizeof(T)); ++j) cv.t[j] = in[j];
+  return cv.u;
+}
+
+// part = part OP x[i] — the PARTIAL_SUMS loop body (corpus.py:219-247).
+template <class T, int OP> struct ReduceBody {
+  static constexpr int V = 16 / sizeof(T);
+  const T *__restrict__ x;
+  T acc[V];
+  OMPRT_D explicit ReduceBody(const T *x_) : x(x_) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[j] = Red<OP, T>::identity();
+  }
+  OMPRT_D bool head_ok(int64_t i) const { return (((uintptr_t)(x + i)) & 15) == 0; }
+  OMPRT_D void scalar(int64_t i) { acc[0] = Red<OP, T>::apply(acc[0], x[i]); }
+  template <int U> OMPRT_D void vecs(const int64_t (&e)[U]) {
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = ld_stream_v4(x + e[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      T t[V];
+      unpack<T>(r[u], t);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = Red<OP, T>::apply(acc[j], t[j]);
+    }
+  }
+  OMPRT_D T total() const {
+    T v = acc[0];
+#pragma unroll
+    for (int j = 1; j < V; ++j) v = Red<OP, T>::apply(v, acc[j]);
+    return v;
+  }
+};
+
+// part = fma(x[i], y[i], part) — fp64 dot (config 5).
+struct DotBody {
+  static constexpr int V = 2;
+  const double *__restrict__ x;
+  const double *__restrict__ y;
+  double acc[2];
+  OMPRT_D DotBody(const double *x_, const double *y_) : x(x_), y(y_) { acc[0] = acc[1] = 0.0; }
+  OMPRT_D bool head_ok(int64_t i) const {
+    return ((((uintptr_t)(x + i)) | ((uintptr_t)(y + i))) & 15) == 0;
+  }
+  OMPRT_D void scalar(int64_t i) { acc[0] = __fma_rn(x[i], y[i], acc[0]); }
+  template <int U> OMPRT_D void vecs(const int64_t (&e)[U]) {
+    uint4 rx[U], ry[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      rx[u] = ld_stream_v4(x + e[u]);
+      ry[u] = ld_stream_v4(y + e[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double a[2], b[2];
+      unpack<double>(rx[u], a);
+      unpack<double>(ry[u], b);
+      acc[0] = __fma_rn(a[0], b[0], acc[0]);
+      acc[1] = __fma_rn(a[1], b[1], acc[1]);
+    }
+  }
+  OMPRT_D double total() const { return acc[0] + acc[1]; }
+};
+
+// y[i] = fmaf(a, x[i], y[i]); mx = max(mx, y[i]); mn = min(mn, y[i]) (config 3).
+struct AxpyBody {
+  static constexpr int V = 4;
+  float a;
+  const float *__restrict__ x;
+  float *__restrict__ y;
+  float mx[4], mn[4];
+  OMPRT_D AxpyBody(float a_, const float *x_, float *y_) : a(a_), x(x_), y(y_) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mx[j] = Limits<float>::lowest();
+      mn[j] = Limits<float>::highest();
+    }
+  }
+  OMPRT_D bool head_ok(int64_t i) const {
+    return ((((uintptr_t)(x + i)) | ((uintptr_t)(y + i))) & 15) == 0;
+  }
+  OMPRT_D void scalar(int64_t i) {
+    const float v = __fmaf_rn(a, x[i], y[i]);
+    y[i] = v;
+    mx[0] = Red<OMPRT_OP_MAX, float>::apply(mx[0], v);
+    mn[0] = Red<OMPRT_OP_MIN, float>::apply(mn[0], v);
+  }
+  template <int U> OMPRT_D void vecs(const int64_t (&e)[U]) {
+    uint4 rx[U], ry[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      rx[u] = ld_stream_v4(x + e[u]);
+      ry[u] = ld_rw_v4(y + e[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float xv[4], yv[4];
+      unpack<float>(rx[u], xv);
+      unpack<float>(ry[u], yv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        yv[j] = __fmaf_rn(a, xv[j], yv[j]);
+        mx[j] = Red<OMPRT_OP_MAX, float>::apply(mx[j], yv[j]);
+        mn[j] = Red<OMPRT_OP_MIN, float>::apply(mn[j], yv[j]);
+      }
+      st_stream_v4(y + e[u], pack<float>(yv));
+    }
+  }
+  OMPRT_D float max_total() const {
+    float v = mx[0];
+#pragma unroll
+    for (int j = 1; j < 4; ++j) v = Red<OMPRT_OP_MAX, float>::apply(v, mx[j]);
+    return v;
+  }
+  OMPRT_D float min_total() const {
+    float v = mn[0];
+#pragma unroll
+    for (int j = 1; j < 4; ++j) v = Red<OMPRT_OP_MIN, float>::apply(v, mn[j]);
+    return v;
+  }
+};
+
+// ------------------------------------------------------------------ kernels
+
+struct LoopArgs {
+  int64_t lb, ub, chunk;
+  int sched;
+};
+
+template <class T, int OP, int U>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_reduce(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
+  __shared__ T scratch[32];
+  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  ReduceBody<T, OP> body(x);
+  run_team<U>(body, s, threadIdx.x, blockDim.x);
+  const T team_val = block_reduce<OP, T>(body.total(), scratch, blockDim.x);
+  T *partials = (T *)ws.team_partials;
+  if (teams_ticket<OP, T>(team_val, partials, ws.ticket)) {
+    const T v = combine_team_partials<OP, T>(partials, scratch);
+    if (threadIdx.x == 0) *out = Red<OP, T>::apply(*out, v);
+  }
+}
+
+// Sequential in-order fold used by ORDERED mode's final combine:
+// acc = ((init OP p0) OP p1) ... — the fallback's atomic order, team-major and
+// tid-minor (host.py:567-582, _atomic_step host.py:810-837).
+template <int OP, class T> OMPRT_D T fold_in_order(T acc, const T *p, int64_t n) {
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    T v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = ld_cg(p + i + k);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = Red<OP, T>::apply(acc, v[k]);
+  }
+  for (; i < n; ++i) acc = Red<OP, T>::apply(acc, ld_cg(p + i));
+  return acc;
+}
+
+template <class T, int OP>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_reduce_ordered(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
+  T part = Red<OP, T>::identity();
+  run_thread_chunks(la.sched, la.lb, la.ub, la.chunk,
+                    [&](int64_t i) { part = Red<OP, T>::apply(part, x[i]); });
+  T *tp = (T *)ws.thread_partials;
+  tp[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = part;
+  __syncthreads();
+  if (teams_ticket<OP, T>(part, (T *)ws.team_partials, ws.ticket) && threadIdx.x == 0) {
+    *out = fold_in_order<OP, T>(*out, tp, (int64_t)gridDim.x * blockDim.x);
+  }
+}
+
+template <int U>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_dot(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la, Workspace ws,
+          double *out) {
+  __shared__ double scratch[32];
+  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  DotBody body(x, y);
+  run_team<U>(body, s, threadIdx.x, blockDim.x);
+  const double team_val = block_reduce<OMPRT_OP_ADD, double>(body.total(), scratch, blockDim.x);
+  double *partials = (double *)ws.team_partials;
+  if (teams_ticket<OMPRT_OP_ADD, double>(team_val, partials, ws.ticket)) {
+    const double v = combine_team_partials<OMPRT_OP_ADD, double>(partials, scratch);
+    if (threadIdx.x == 0) *out = *out + v;
+  }
+}
+
+__global__ void __launch_bounds__(kMaxThreads)
+    k_dot_ordered(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
+                  Workspace ws, double *out) {
+  double part = 0.0;
+  run_thread_chunks(la.sched, la.lb, la.ub, la.chunk,
+                    [&](int64_t i) { part = __fma_rn(x[i], y[i], part); });
+  double *tp = (double *)ws.thread_partials;
+  tp[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = part;
+  __syncthreads();
+  if (teams_ticket<OMPRT_OP_ADD, double>(part, (double *)ws.team_partials, ws.ticket) &&
+      threadIdx.x == 0) {
+    *out = fold_in_order<OMPRT_OP_ADD, double>(*out, tp, (int64_t)gridDim.x * blockDim.x);
+  }
+}
+
+// Two partial arrays (max, min) share one ticket: slots = 2 in ws_bytes.
+template <int U>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_axpy_minmax(float a, const float *__restrict__ x, float *__restrict__ y, LoopArgs la,
+                  Workspace ws, float *out_max, float *out_min) {
+  __shared__ float scratch[32];
+  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  AxpyBody body(a, x, y);
+  run_team<U>(body, s, threadIdx.x, blockDim.x);
+  const float tmax = block_reduce<OMPRT_OP_MAX, float>(body.max_total(), scratch, blockDim.x);
+  const float tmin = block_reduce<OMPRT_OP_MIN, float>(body.min_total(), scratch, blockDim.x);
+  float *pmax = (float *)ws.team_partials;
+  float *pmin = pmax + gridDim.x;
+  if (threadIdx.x == 0) pmin[blockIdx.x] = tmin;
+  if (teams_ticket<OMPRT_OP_MAX, float>(tmax, pmax, ws.ticket)) {
+    const float vmax = combine_team_partials<OMPRT_OP_MAX, float>(pmax, scratch);
+    const float vmin = combine_team_partials<OMPRT_OP_MIN, float>(pmin, scratch);
+    if (threadIdx.x == 0) {
+      *out_max = Red<OMPRT_OP_MAX, float>::apply(*out_max, vmax);
+      *out_min = Red<OMPRT_OP_MIN, float>::apply(*out_min, vmin);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kMaxThreads)
+    k_axpy_minmax_ordered(float a, const float *__restrict__ x, float *__restrict__ y,
+                          LoopArgs la, Workspace ws, float *out_max, float *out_min) {
+  float mx = Limits<float>::lowest(), mn = Limits<float>::highest();
+  run_thread_chunks(la.sched, la.lb, la.ub, la.chunk, [&](int64_t i) {
+    const float v = __fmaf_rn(a, x[i], y[i]);
+    y[i] = v;
+    mx = Red<OMPRT_OP_MAX, float>::apply(mx, v);
+    mn = Red<OMPRT_OP_MIN, float>::apply(mn, v);
+  });
+  const int64_t n = (int64_t)gridDim.x * blockDim.x;
+  float *tmax = (float *)ws.thread_partials;
+  float *tmin = tmax + n;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  tmax[g] = mx;
+  tmin[g] = mn;
+  __syncthreads();
+  if (teams_ticket<OMPRT_OP_MAX, float>(mx, (float *)ws.team_partials, ws.ticket) &&
+      threadIdx.x == 0) {
+    *out_max = fold_in_order<OMPRT_OP_MAX, float>(*out_max, tmax, n);
+    *out_min = fold_in_order<OMPRT_OP_MIN, float>(*out_min, tmin, n);
+  }
+}
+
+// Every device thread runs the schedule's init routine (for_static_init,
+// runtime.mc:193-203, and the chunked / distribute variants) and dumps it.
+__global__ void k_bounds_dump(LoopArgs la, int64_t *__restrict__ out) {
+  const Bounds b = schedule_init(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x,
+                                 threadIdx.x, blockDim.x);
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  out[4 * g + 0] = b.lower;
+  out[4 * g + 1] = b.upper;
+  out[4 * g + 2] = b.stride;
+  out[4 * g + 3] = b.last;
+}
+
+template <class T>
+__global__ void k_fill(T *__restrict__ x, int64_t n, uint64_t seed, int k, int64_t offset) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool aligned = (((uintptr_t)x) & 15) == 0;
+  const int64_t nvec = aligned ? n / V : 0;
+  for (int64_t v = g; v < nvec; v += nthr) {
+    T t[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+      t[j] = gen_value<T>(gen_bits(seed, k, (uint64_t)(offset + v * V + j)));
+    st_stream_v4(x + v * V, pack<T>(t));
+  }
+  for (int64_t i = nvec * V + g; i < n; i += nthr)
+    x[i] = gen_value<T>(gen_bits(seed, k, (uint64_t)(offset + i)));
+}
+
+template <class T, int OP> __global__ void k_combine(const T *p, int count, T *out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    T acc = *out;
+    for (int i = 0; i < count; ++i) acc = Red<OP, T>::apply(acc, p[i]);
+    *out = acc;
+  }
+}
+
+}  // namespace omprt

@@ -1,0 +1,537 @@
+// omprt_b200.cu — the C ABI (include/omprt_b200.h) over the sm_100a kernels.
+// Single translation unit: the device runtime, every kernel and the host
+// entry points, so the trap word is one device symbol.
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+
+#include "generic.cuh"
+
+using namespace omprt;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  return code;
+}
+
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(OMPRT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return OMPRT_OK;
+}
+
+#define OMPRT_CUDA(call)                                                                   \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess) return fail(OMPRT_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int g_unroll = 4;  // tuning knob: vectors in flight per lane per iteration
+
+int check_grid(int teams, int threads) {
+  if (teams < 1) return fail(OMPRT_EINVAL, "teams must be >= 1 (got %d)", teams);
+  if (threads < 1 || threads > kMaxThreads)
+    return fail(OMPRT_EINVAL, "threads must lie in 1..%d (got %d)", kMaxThreads, threads);
+  return OMPRT_OK;
+}
+
+int check_sched(int sched, int64_t chunk) {
+  if (sched < OMPRT_SCHED_STATIC || sched > OMPRT_SCHED_DISTRIBUTE_CHUNKED)
+    return fail(OMPRT_EINVAL, "unknown schedule %d", sched);
+  if ((sched == OMPRT_SCHED_STATIC_CHUNKED || sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED) &&
+      chunk < 1)
+    return fail(OMPRT_EINVAL, "chunked schedule needs chunk >= 1 (got %lld)", (long long)chunk);
+  return OMPRT_OK;
+}
+
+// ---------------------------------------------------------------- dispatch
+
+template <class T, int OP>
+int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode, Workspace w,
+                    void *out, cudaStream_t st) {
+  const T *xp = (const T *)x;
+  T *op = (T *)out;
+  if (mode == OMPRT_MODE_ORDERED) {
+    k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
+  } else if (g_unroll >= 8) {
+    k_reduce<T, OP, 8><<<teams, threads, 0, st>>>(xp, la, w, op);
+  } else if (g_unroll <= 2) {
+    k_reduce<T, OP, 2><<<teams, threads, 0, st>>>(xp, la, w, op);
+  } else {
+    k_reduce<T, OP, 4><<<teams, threads, 0, st>>>(xp, la, w, op);
+  }
+  return check_launch("omprt_reduce");
+}
+
+template <class T>
+int launch_reduce_op(int op, const void *x, LoopArgs la, int teams, int threads, int mode,
+                     Workspace w, void *out, cudaStream_t st) {
+  switch (op) {
+    case OMPRT_OP_ADD:
+      return launch_reduce_t<T, OMPRT_OP_ADD>(x, la, teams, threads, mode, w, out, st);
+    case OMPRT_OP_MAX:
+      return launch_reduce_t<T, OMPRT_OP_MAX>(x, la, teams, threads, mode, w, out, st);
+    case OMPRT_OP_MIN:
+      return launch_reduce_t<T, OMPRT_OP_MIN>(x, la, teams, threads, mode, w, out, st);
+  }
+  return fail(OMPRT_EINVAL, "unknown reduction op %d", op);
+}
+
+size_t dtype_size(int dtype) {
+  switch (dtype) {
+    case OMPRT_I32:
+    case OMPRT_U32:
+    case OMPRT_F32:
+      return 4;
+    case OMPRT_I64:
+    case OMPRT_U64:
+    case OMPRT_F64:
+      return 8;
+  }
+  return 0;
+}
+
+template <template <class> class F, class... A> int by_dtype(int dtype, A... a) {
+  switch (dtype) {
+    case OMPRT_I32:
+      return F<int32_t>::run(a...);
+    case OMPRT_U32:
+      return F<uint32_t>::run(a...);
+    case OMPRT_I64:
+      return F<int64_t>::run(a...);
+    case OMPRT_U64:
+      return F<uint64_t>::run(a...);
+    case OMPRT_F32:
+      return F<float>::run(a...);
+    case OMPRT_F64:
+      return F<double>::run(a...);
+  }
+  return fail(OMPRT_EINVAL, "unknown dtype %d", dtype);
+}
+
+template <class T> struct ReduceF {
+  static int run(int op, const void *x, LoopArgs la, int teams, int threads, int mode,
+                 Workspace w, void *out, cudaStream_t st) {
+    return launch_reduce_op<T>(op, x, la, teams, threads, mode, w, out, st);
+  }
+};
+
+template <class T> struct FillF {
+  static int run(void *x, int64_t n, uint64_t seed, int k, int64_t offset, cudaStream_t st) {
+    if (n <= 0) return OMPRT_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t vecs = n / (int64_t)(16 / sizeof(T)) + 1;
+    int64_t blocks = (vecs + 255) / 256;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    k_fill<T><<<(unsigned)blocks, 256, 0, st>>>((T *)x, n, seed, k, offset);
+    return check_launch("omprt_fill");
+  }
+};
+
+template <class T> struct CombineF {
+  static int run(int op, const void *p, int count, void *out, cudaStream_t st) {
+    switch (op) {
+      case OMPRT_OP_ADD:
+        k_combine<T, OMPRT_OP_ADD><<<1, 32, 0, st>>>((const T *)p, count, (T *)out);
+        break;
+      case OMPRT_OP_MAX:
+        k_combine<T, OMPRT_OP_MAX><<<1, 32, 0, st>>>((const T *)p, count, (T *)out);
+        break;
+      case OMPRT_OP_MIN:
+        k_combine<T, OMPRT_OP_MIN><<<1, 32, 0, st>>>((const T *)p, count, (T *)out);
+        break;
+      default:
+        return fail(OMPRT_EINVAL, "unknown reduction op %d", op);
+    }
+    return check_launch("omprt_combine_partials");
+  }
+};
+
+template <class T> struct AtomicF {
+  static int run(int kind, const uint64_t *ops, const uint64_t *desired, void *cell,
+                 uint64_t *old, int teams, int threads, cudaStream_t st) {
+    k_atomic_probe<T><<<teams, threads, 0, st>>>(kind, ops, desired, (T *)cell, old);
+    return check_launch("omprt_atomic_probe");
+  }
+  static int apply(int kind, void *cells, const uint64_t *ops, const uint64_t *desired,
+                   uint64_t *old, int64_t n, cudaStream_t st) {
+    if (n <= 0) return OMPRT_OK;
+    const int64_t blocks = (n + 255) / 256;
+    k_atomic_apply<T><<<(unsigned)blocks, 256, 0, st>>>(kind, (T *)cells, ops, desired, old, n);
+    return check_launch("omprt_atomic_apply");
+  }
+};
+
+int check_atomic(int kind, int dtype, const uint64_t *desired) {
+  if (kind < OMPRT_ATOMIC_ADD || kind > OMPRT_ATOMIC_INC)
+    return fail(OMPRT_EINVAL, "unknown atomic kind %d", kind);
+  if (dtype != OMPRT_I32 && dtype != OMPRT_U32 && dtype != OMPRT_I64 && dtype != OMPRT_U64)
+    return fail(OMPRT_EINVAL, "atomics take i32/u32/i64/u64 (got dtype %d)", dtype);
+  if (kind == OMPRT_ATOMIC_INC && dtype != OMPRT_U32)
+    return fail(OMPRT_EINVAL, "atomic_inc is u32 only (runtime.mc:175-186)");
+  if (kind == OMPRT_ATOMIC_CAS && !desired) return fail(OMPRT_EINVAL, "CAS needs desired values");
+  return OMPRT_OK;
+}
+
+template <class T, int OP>
+int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, int ordered,
+                     int64_t pad, ArenaCfg cfg, Workspace w, void *out, int64_t *offs,
+                     cudaStream_t st) {
+  auto kern = k_generic<T, OP, 4>;
+  const size_t smem = (size_t)cfg.capacity;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess)
+      return fail(OMPRT_ECUDA, "generic: smem attribute: %s", cudaGetErrorString(e));
+  }
+  kern<<<teams, 32 + P, smem, st>>>((const T *)x, lb, ub, P, ordered, pad, cfg, w, (T *)out, offs);
+  return check_launch("omprt_generic_reduce");
+}
+
+template <class T>
+int launch_generic_op(int op, const void *x, int64_t lb, int64_t ub, int teams, int P,
+                      int ordered, int64_t pad, ArenaCfg cfg, Workspace w, void *out,
+                      int64_t *offs, cudaStream_t st) {
+  switch (op) {
+    case OMPRT_OP_ADD:
+      return launch_generic_t<T, OMPRT_OP_ADD>(x, lb, ub, teams, P, ordered, pad, cfg, w, out,
+                                               offs, st);
+    case OMPRT_OP_MAX:
+      return launch_generic_t<T, OMPRT_OP_MAX>(x, lb, ub, teams, P, ordered, pad, cfg, w, out,
+                                               offs, st);
+    case OMPRT_OP_MIN:
+      return launch_generic_t<T, OMPRT_OP_MIN>(x, lb, ub, teams, P, ordered, pad, cfg, w, out,
+                                               offs, st);
+  }
+  return fail(OMPRT_EINVAL, "unknown reduction op %d", op);
+}
+
+size_t generic_ws_core(int teams) { return ws_bytes(teams, 0, OMPRT_MODE_SPMD, 1); }
+
+// host-buffer entry cache
+std::mutex g_host_mu;
+void *g_host_x = nullptr;
+size_t g_host_x_bytes = 0;
+void *g_host_ws = nullptr;
+size_t g_host_ws_bytes = 0;
+void *g_host_out = nullptr;
+cudaStream_t g_host_stream = nullptr;
+
+}  // namespace
+
+// ======================================================================= ABI
+
+extern "C" {
+
+const char *omprt_version(void) { return "omprt_b200 0.1.0 sm_100a"; }
+
+const char *omprt_last_error(void) { return t_last_error.c_str(); }
+
+int omprt_device_init(int device) {
+  OMPRT_CUDA(cudaSetDevice(device));
+  TrapWord z = {0, 0, 0, 0};
+  OMPRT_CUDA(cudaMemcpyToSymbol(g_trap, &z, sizeof(z)));
+  return OMPRT_OK;
+}
+
+int omprt_num_sms(void) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(OMPRT_ECUDA, "no CUDA device");
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return fail(OMPRT_ECUDA, "cudaDeviceGetAttribute failed");
+  return sms;
+}
+
+int omprt_check_trap(void *stream, int *kind, int *code, int *team, int *thread) {
+  OMPRT_CUDA(cudaStreamSynchronize(S(stream)));
+  TrapWord t;
+  OMPRT_CUDA(cudaMemcpyFromSymbol(&t, g_trap, sizeof(t)));
+  if (kind) *kind = t.kind;
+  if (code) *code = t.code;
+  if (team) *team = t.team;
+  if (thread) *thread = t.thread;
+  if (t.kind == 0) return OMPRT_OK;
+  TrapWord z = {0, 0, 0, 0};
+  OMPRT_CUDA(cudaMemcpyToSymbol(g_trap, &z, sizeof(z)));
+  return OMPRT_TRAP;
+}
+
+int omprt_set_unroll(int unroll) {
+  if (unroll != 2 && unroll != 4 && unroll != 8)
+    return fail(OMPRT_EINVAL, "unroll must be 2, 4 or 8 (got %d)", unroll);
+  g_unroll = unroll;
+  return OMPRT_OK;
+}
+
+int omprt_static_bounds(int64_t lb, int64_t ub, int64_t tid, int64_t nthreads, int64_t *my_lb,
+                        int64_t *my_ub) {
+  if (nthreads == 0) {
+    t_last_error = "DivideByZero: sdiv.i64 by zero";
+    return OMPRT_TRAP;
+  }
+  int64_t a, b;
+  static_bounds(lb, ub, tid, nthreads, a, b);
+  if (my_lb) *my_lb = a;
+  if (my_ub) *my_ub = b;
+  return OMPRT_OK;
+}
+
+int omprt_bounds_dump(int64_t lb, int64_t ub, int sched, int64_t chunk, int teams, int threads,
+                      int64_t *d_out, void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  if (!d_out) return fail(OMPRT_EINVAL, "bounds_dump: null output");
+  LoopArgs la{lb, ub, chunk, sched};
+  k_bounds_dump<<<teams, threads, 0, S(stream)>>>(la, d_out);
+  return check_launch("omprt_bounds_dump");
+}
+
+size_t omprt_reduce_workspace_bytes(int teams, int threads, int mode) {
+  return ws_bytes(teams < 1 ? 1 : teams, threads < 1 ? 1 : threads, mode, 2);
+}
+
+int omprt_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int sched,
+                 int64_t chunk, int teams, int threads, int mode, void *d_ws, void *d_out,
+                 void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  if (!d_ws || !d_out || (!d_x && ub >= lb))
+    return fail(OMPRT_EINVAL, "reduce: null device pointer");
+  if (mode != OMPRT_MODE_SPMD && mode != OMPRT_MODE_ORDERED)
+    return fail(OMPRT_EINVAL, "unknown mode %d", mode);
+  LoopArgs la{lb, ub, chunk, sched};
+  Workspace w = ws_carve(d_ws, teams, 2);
+  return by_dtype<ReduceF>(dtype, op, d_x, la, teams, threads, mode, w, d_out, S(stream));
+}
+
+int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t ub, int sched,
+                      int64_t chunk, int teams, int threads, int mode, void *d_ws, float *d_max,
+                      float *d_min, void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  if (!d_ws || !d_max || !d_min || ((!d_x || !d_y) && ub >= lb))
+    return fail(OMPRT_EINVAL, "axpy_minmax: null device pointer");
+  LoopArgs la{lb, ub, chunk, sched};
+  Workspace w = ws_carve(d_ws, teams, 2);
+  if (mode == OMPRT_MODE_ORDERED)
+    k_axpy_minmax_ordered<<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+  else
+    k_axpy_minmax<4><<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+  return check_launch("omprt_axpy_minmax");
+}
+
+int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int sched,
+              int64_t chunk, int teams, int threads, int mode, void *d_ws, double *d_out,
+              void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  if (!d_ws || !d_out || ((!d_x || !d_y) && ub >= lb))
+    return fail(OMPRT_EINVAL, "dot: null device pointer");
+  LoopArgs la{lb, ub, chunk, sched};
+  Workspace w = ws_carve(d_ws, teams, 2);
+  if (mode == OMPRT_MODE_ORDERED)
+    k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+  else if (g_unroll >= 8)
+    k_dot<8><<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+  else
+    k_dot<4><<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+  return check_launch("omprt_dot");
+}
+
+int omprt_combine_partials(const void *d_partials, int count, int dtype, int op, void *d_out,
+                           void *stream) {
+  if (count < 0 || !d_out || (count > 0 && !d_partials))
+    return fail(OMPRT_EINVAL, "combine_partials: bad arguments");
+  return by_dtype<CombineF>(dtype, op, d_partials, count, d_out, S(stream));
+}
+
+size_t omprt_generic_workspace_bytes(int teams, int par_threads, int heap_fallback,
+                                     int64_t heap_bytes_per_team) {
+  (void)par_threads;
+  size_t b = generic_ws_core(teams < 1 ? 1 : teams);
+  if (heap_fallback) b += (size_t)(teams < 1 ? 1 : teams) * (size_t)heap_bytes_per_team;
+  return (b + 255) & ~(size_t)255;
+}
+
+int omprt_generic_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int teams,
+                         int par_threads, int ordered, int64_t pad_bytes, int heap_fallback,
+                         int64_t heap_bytes_per_team, void *d_ws, void *d_out,
+                         int64_t *d_team_offsets, void *stream) {
+  if (teams < 1) return fail(OMPRT_EINVAL, "teams must be >= 1");
+  if (par_threads < 32 || par_threads % 32 != 0 || par_threads + 32 > kMaxThreads)
+    return fail(OMPRT_EINVAL, "par_threads must be a multiple of 32 in 32..%d (got %d)",
+                kMaxThreads - 32, par_threads);
+  if (pad_bytes < 0 || (heap_fallback && heap_bytes_per_team < 0))
+    return fail(OMPRT_EINVAL, "generic: negative sizes");
+  if (!d_ws || !d_out || (!d_x && ub >= lb))
+    return fail(OMPRT_EINVAL, "generic: null device pointer");
+  Workspace w = ws_carve(d_ws, teams, 1);
+  ArenaCfg cfg;
+  cfg.capacity = OMPRT_ARENA_CAPACITY;
+  cfg.heap_fallback = heap_fallback ? 1 : 0;
+  cfg.heap_per_team = heap_fallback ? heap_bytes_per_team : 0;
+  cfg.heap = heap_fallback ? (unsigned char *)d_ws + generic_ws_core(teams) : nullptr;
+  switch (dtype) {
+    case OMPRT_I64:
+      return launch_generic_op<int64_t>(op, d_x, lb, ub, teams, par_threads, ordered, pad_bytes,
+                                        cfg, w, d_out, d_team_offsets, S(stream));
+    case OMPRT_U64:
+      return launch_generic_op<uint64_t>(op, d_x, lb, ub, teams, par_threads, ordered,
+                                         pad_bytes, cfg, w, d_out, d_team_offsets, S(stream));
+    case OMPRT_F64:
+      return launch_generic_op<double>(op, d_x, lb, ub, teams, par_threads, ordered, pad_bytes,
+                                       cfg, w, d_out, d_team_offsets, S(stream));
+  }
+  return fail(OMPRT_EINVAL, "generic_reduce: dtype must be I64, U64 or F64 (got %d)", dtype);
+}
+
+int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads,
+                       int caller_tid, int64_t capacity, int heap_fallback,
+                       int64_t heap_bytes_per_team, void *d_heap, int64_t *d_results,
+                       void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads))) return rc;
+  if (nops < 0 || (nops > 0 && (!d_script || !d_results)))
+    return fail(OMPRT_EINVAL, "arena_replay: bad script");
+  if (capacity < 0 || capacity > OMPRT_ARENA_CAPACITY || capacity % 16 != 0)
+    return fail(OMPRT_EINVAL, "arena capacity must be a multiple of 16 in 0..%d",
+                OMPRT_ARENA_CAPACITY);
+  if (caller_tid < 0 || caller_tid >= threads)
+    return fail(OMPRT_EINVAL, "caller_tid must lie in 0..threads-1");
+  if (heap_fallback && (!d_heap || heap_bytes_per_team < 0))
+    return fail(OMPRT_EINVAL, "heap fallback needs a heap buffer");
+  if (nops == 0) return OMPRT_OK;
+  ArenaCfg cfg;
+  cfg.capacity = capacity;
+  cfg.heap_fallback = heap_fallback ? 1 : 0;
+  cfg.heap_per_team = heap_fallback ? heap_bytes_per_team : 0;
+  cfg.heap = (unsigned char *)d_heap;
+  const size_t smem = (size_t)(capacity > 0 ? capacity : 16);
+  if (smem > 48 * 1024)
+    OMPRT_CUDA(cudaFuncSetAttribute(k_arena_replay, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  k_arena_replay<<<teams, threads, smem, S(stream)>>>(d_script, nops, caller_tid, cfg, d_results);
+  if ((rc = check_launch("omprt_arena_replay"))) return rc;
+  int kind = 0;
+  return omprt_check_trap(stream, &kind, nullptr, nullptr, nullptr);
+}
+
+int omprt_atomic_probe(int kind, int dtype, const uint64_t *d_operands, const uint64_t *d_desired,
+                       uint64_t *d_cell, uint64_t *d_old, int teams, int threads, void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads))) return rc;
+  if ((rc = check_atomic(kind, dtype, d_desired))) return rc;
+  if (!d_operands || !d_cell || !d_old) return fail(OMPRT_EINVAL, "atomic_probe: null pointer");
+  switch (dtype) {
+    case OMPRT_I32:
+      return AtomicF<int32_t>::run(kind, d_operands, d_desired, d_cell, d_old, teams, threads,
+                                   S(stream));
+    case OMPRT_U32:
+      return AtomicF<uint32_t>::run(kind, d_operands, d_desired, d_cell, d_old, teams, threads,
+                                    S(stream));
+    case OMPRT_I64:
+      return AtomicF<int64_t>::run(kind, d_operands, d_desired, d_cell, d_old, teams, threads,
+                                   S(stream));
+    default:
+      return AtomicF<uint64_t>::run(kind, d_operands, d_desired, d_cell, d_old, teams, threads,
+                                    S(stream));
+  }
+}
+
+int omprt_atomic_apply(int kind, int dtype, uint64_t *d_cells, const uint64_t *d_operands,
+                       const uint64_t *d_desired, uint64_t *d_old, int64_t n, void *stream) {
+  int rc;
+  if ((rc = check_atomic(kind, dtype, d_desired))) return rc;
+  if (n < 0 || (n > 0 && (!d_cells || !d_operands || !d_old)))
+    return fail(OMPRT_EINVAL, "atomic_apply: bad arguments");
+  switch (dtype) {
+    case OMPRT_I32:
+      return AtomicF<int32_t>::apply(kind, d_cells, d_operands, d_desired, d_old, n, S(stream));
+    case OMPRT_U32:
+      return AtomicF<uint32_t>::apply(kind, d_cells, d_operands, d_desired, d_old, n, S(stream));
+    case OMPRT_I64:
+      return AtomicF<int64_t>::apply(kind, d_cells, d_operands, d_desired, d_old, n, S(stream));
+    default:
+      return AtomicF<uint64_t>::apply(kind, d_cells, d_operands, d_desired, d_old, n, S(stream));
+  }
+}
+
+int omprt_fill(void *d_x, int64_t n, int dtype, uint64_t seed, int k, int64_t offset,
+               void *stream) {
+  if (n < 0 || (n > 0 && !d_x)) return fail(OMPRT_EINVAL, "fill: bad arguments");
+  return by_dtype<FillF>(dtype, d_x, n, seed, k, offset, S(stream));
+}
+
+int omprt_reduce_host(const void *h_x, int64_t n, int dtype, int op, int sched, int64_t chunk,
+                      int teams, int threads, int mode, void *h_out) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  const size_t es = dtype_size(dtype);
+  if (!es) return fail(OMPRT_EINVAL, "unknown dtype %d", dtype);
+  if (n < 0 || !h_out || (n > 0 && !h_x)) return fail(OMPRT_EINVAL, "reduce_host: bad arguments");
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  if (!g_host_stream) OMPRT_CUDA(cudaStreamCreateWithFlags(&g_host_stream, cudaStreamNonBlocking));
+  const size_t xbytes = (size_t)n * es;
+  if (xbytes > g_host_x_bytes) {
+    if (g_host_x) cudaFree(g_host_x);
+    g_host_x = nullptr;
+    g_host_x_bytes = 0;
+    if (cudaMalloc(&g_host_x, xbytes) != cudaSuccess)
+      return fail(OMPRT_ENOMEM, "reduce_host: cannot allocate %zu device bytes", xbytes);
+    g_host_x_bytes = xbytes;
+  }
+  const size_t wsb = omprt_reduce_workspace_bytes(teams, threads, mode);
+  if (wsb > g_host_ws_bytes) {
+    if (g_host_ws) cudaFree(g_host_ws);
+    g_host_ws = nullptr;
+    g_host_ws_bytes = 0;
+    if (cudaMalloc(&g_host_ws, wsb) != cudaSuccess)
+      return fail(OMPRT_ENOMEM, "reduce_host: cannot allocate workspace");
+    OMPRT_CUDA(cudaMemset(g_host_ws, 0, wsb));
+    g_host_ws_bytes = wsb;
+  }
+  if (!g_host_out) OMPRT_CUDA(cudaMalloc(&g_host_out, 16));
+  cudaStream_t st = g_host_stream;
+  // copy-in (tgt_target host.py:276-281)
+  if (xbytes) OMPRT_CUDA(cudaMemcpyAsync(g_host_x, h_x, xbytes, cudaMemcpyHostToDevice, st));
+  OMPRT_CUDA(cudaMemcpyAsync(g_host_out, h_out, es, cudaMemcpyHostToDevice, st));
+  rc = omprt_reduce(g_host_x, 0, n - 1, dtype, op, sched, chunk, teams, threads, mode, g_host_ws,
+                    g_host_out, st);
+  if (rc) return rc;
+  // copy-out only on status 0 (host.py:293-295)
+  unsigned char res[16];
+  OMPRT_CUDA(cudaMemcpyAsync(res, g_host_out, es, cudaMemcpyDeviceToHost, st));
+  OMPRT_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(h_out, res, es);
+  return OMPRT_OK;
+}
+
+int omprt_release_host_cache(void) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  if (g_host_x) cudaFree(g_host_x);
+  if (g_host_ws) cudaFree(g_host_ws);
+  if (g_host_out) cudaFree(g_host_out);
+  g_host_x = g_host_ws = g_host_out = nullptr;
+  g_host_x_bytes = g_host_ws_bytes = 0;
+  return OMPRT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,349 @@
+"""Device-side entry points of the data-parallel core, over torch tensors.
+
+Every function here launches a kernel of libomprt_b200.so on the tensors'
+CUDA device and current stream; none has a CPU path.  Iteration spaces are
+inclusive [lb, ub] and index the input arrays directly (x[i]), exactly like
+the reference's `for_static_init(lb, ub, ...)` loops (runtime.mc:193-203).
+
+Names follow the OpenMP device runtime the paper rewrites:
+  bounds_dump        __kmpc_for_static_init / __kmpc_distribute_static_init
+  reduce             target teams distribute parallel for reduction(op: cell)
+  axpy_minmax        the same construct over y = a*x + y with max/min
+  dot                fp64 dot product reduction
+  generic_reduce     generic-mode region: __kmpc_alloc_shared + nested parallel reduce
+  arena_replay       __kmpc_alloc_shared / __kmpc_free_shared scripts
+  atomic_probe       the seq_cst atomic intrinsics on one cell
+  atomic_apply       batched step_* semantics
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+_TORCH_DTYPE = {
+    _lib.I32: torch.int32, _lib.U32: torch.uint32, _lib.I64: torch.int64,
+    _lib.U64: torch.uint64, _lib.F32: torch.float32, _lib.F64: torch.float64,
+}
+_FROM_TORCH = {v: k for k, v in _TORCH_DTYPE.items()}
+
+
+def dtype_code(dtype) -> int:
+    if isinstance(dtype, int):
+        return dtype
+    if isinstance(dtype, str):
+        return _lib.DTYPE_NAMES[dtype]
+    return _FROM_TORCH[dtype]
+
+
+def torch_dtype(code: int) -> torch.dtype:
+    return _TORCH_DTYPE[code]
+
+
+def _code(table: dict, v) -> int:
+    return v if isinstance(v, int) else table[v]
+
+
+def _stream(t: torch.Tensor) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _dev(t: torch.Tensor) -> torch.device:
+    if not t.is_cuda:
+        raise ValueError("tensors must live on a CUDA device (there is no CPU path)")
+    _lib.ensure_device(t.device.index or 0)
+    return t.device
+
+
+def _p(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def num_sms() -> int:
+    return check(_lib.load().omprt_num_sms(), "omprt_num_sms")
+
+
+def set_unroll(unroll: int) -> None:
+    check(_lib.load().omprt_set_unroll(unroll), "omprt_set_unroll")
+
+
+@dataclass(frozen=True)
+class Grid:
+    """Launch geometry: num_teams x thread_limit (GridConfig, vgpu.py:50-61)."""
+
+    teams: int
+    threads: int
+
+
+def default_grid(device: torch.device | None = None, threads: int = 1024,
+                 teams_per_sm: int = 2) -> Grid:
+    """A persistent grid: teams_per_sm resident teams on every SM."""
+    if device is not None:
+        _lib.ensure_device(device.index or 0)
+    return Grid(num_sms() * teams_per_sm, threads)
+
+
+# ------------------------------------------------------------------ trap
+
+@dataclass(frozen=True)
+class DeviceTrap:
+    kind: int
+    code: int
+    team: int
+    thread: int
+
+
+def check_trap(device: torch.device) -> DeviceTrap | None:
+    """Synchronise the current stream and fetch/clear the device trap word."""
+    _lib.ensure_device(device.index or 0)
+    L = _lib.load()
+    k, c, tm, th = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    st = check(L.omprt_check_trap(C.c_void_p(torch.cuda.current_stream(device).cuda_stream),
+                                  C.byref(k), C.byref(c), C.byref(tm), C.byref(th)),
+               "omprt_check_trap")
+    if st == _lib.OK:
+        return None
+    return DeviceTrap(k.value, c.value, tm.value, th.value)
+
+
+# ------------------------------------------------------------ worksharing
+
+def static_bounds(lb: int, ub: int, tid: int, nthreads: int) -> tuple[int, int]:
+    """for_static_init / devicert.static_bounds through the library's
+    __host__ __device__ routine (the same code every device thread runs)."""
+    a, b = C.c_int64(), C.c_int64()
+    st = _lib.load().omprt_static_bounds(lb, ub, tid, nthreads, C.byref(a), C.byref(b))
+    if st == _lib.TRAP:
+        raise ZeroDivisionError("for_static_init: nthreads == 0 (DivideByZero trap)")
+    check(st, "omprt_static_bounds")
+    return a.value, b.value
+
+
+def bounds_dump(lb: int, ub: int, sched="static", chunk: int = 1, *, teams: int, threads: int,
+                device="cuda") -> torch.Tensor:
+    """Every device thread's schedule init result: int64 [teams*threads, 4]
+    (lower, upper, stride, last) — see include/omprt_b200.h."""
+    out = torch.empty((teams * threads, 4), dtype=torch.int64, device=device)
+    _dev(out)
+    check(_lib.load().omprt_bounds_dump(lb, ub, _code(_lib.SCHED_NAMES, sched), chunk, teams,
+                                        threads, _p(out), _stream(out)), "omprt_bounds_dump")
+    return out
+
+
+# ------------------------------------------------------------- workspace
+
+_ws_cache: dict[tuple, torch.Tensor] = {}
+
+
+def workspace(device: torch.device, nbytes: int) -> torch.Tensor:
+    """Zeroed device workspace, cached per device (the last-team-finishes
+    ticket self-resets, so reuse across launches on one stream is safe)."""
+    key = (device.type, device.index or 0)
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def reduce_workspace(device: torch.device, teams: int, threads: int, mode: int) -> torch.Tensor:
+    return workspace(device, _lib.load().omprt_reduce_workspace_bytes(teams, threads, mode))
+
+
+# ---------------------------------------------------------------- reduce
+
+def reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = None, sched="static",
+           chunk: int = 1, teams: int | None = None, threads: int | None = None, mode="spmd",
+           out: torch.Tensor | None = None, init=None) -> torch.Tensor:
+    """`#pragma omp target teams distribute parallel for reduction(op: cell)`
+    over x[lb..ub].  Returns the 1-element device tensor `out`, updated in
+    place as out = out OP reduce(x) (the original list item is combined in,
+    like __atomic_add(cell, part) in corpus.py:219-247)."""
+    dev = _dev(x)
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
+    dt = dtype_code(x.dtype)
+    opc = _code(_lib.OP_NAMES, op)
+    m = _code(_lib.MODE_NAMES, mode)
+    if ub is None:
+        ub = lb + x.numel() - 1
+    if ub >= lb and (lb < 0 or ub >= x.numel()):
+        raise IndexError(f"iteration space [{lb}, {ub}] escapes x[0:{x.numel()}]")
+    g = default_grid(dev)
+    teams = teams or g.teams
+    threads = threads or g.threads
+    if out is None:
+        out = torch.zeros(1, dtype=x.dtype, device=dev)
+        if init is not None:
+            out.fill_(init)
+    ws = reduce_workspace(dev, teams, threads, m)
+    check(_lib.load().omprt_reduce(_p(x), lb, ub, dt, opc, _code(_lib.SCHED_NAMES, sched), chunk,
+                                   teams, threads, m, _p(ws), _p(out), _stream(x)),
+          "omprt_reduce")
+    return out
+
+
+def axpy_minmax(a: float, x: torch.Tensor, y: torch.Tensor, *, lb: int = 0, ub: int | None = None,
+                sched="distribute_chunked", chunk: int = 1, teams: int | None = None,
+                threads: int | None = None, mode="spmd",
+                out_max: torch.Tensor | None = None,
+                out_min: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """y[i] = fmaf(a, x[i], y[i]) for i in [lb, ub], fused with max/min of y."""
+    dev = _dev(x)
+    if x.dtype != torch.float32 or y.dtype != torch.float32:
+        raise TypeError("axpy_minmax is fp32")
+    if ub is None:
+        ub = lb + x.numel() - 1
+    g = default_grid(dev)
+    teams = teams or g.teams
+    threads = threads or g.threads
+    m = _code(_lib.MODE_NAMES, mode)
+    if out_max is None:
+        out_max = torch.full((1,), float("-inf"), dtype=torch.float32, device=dev)
+    if out_min is None:
+        out_min = torch.full((1,), float("inf"), dtype=torch.float32, device=dev)
+    ws = reduce_workspace(dev, teams, threads, m)
+    check(_lib.load().omprt_axpy_minmax(C.c_float(a), _p(x), _p(y), lb, ub,
+                                        _code(_lib.SCHED_NAMES, sched), chunk, teams, threads, m,
+                                        _p(ws), _p(out_max), _p(out_min), _stream(x)),
+          "omprt_axpy_minmax")
+    return out_max, out_min
+
+
+def dot(x: torch.Tensor, y: torch.Tensor, *, lb: int = 0, ub: int | None = None,
+        sched="static", chunk: int = 1, teams: int | None = None, threads: int | None = None,
+        mode="spmd", out: torch.Tensor | None = None) -> torch.Tensor:
+    """fp64 dot product reduction: out = out + sum fma(x[i], y[i], part)."""
+    dev = _dev(x)
+    if x.dtype != torch.float64 or y.dtype != torch.float64:
+        raise TypeError("dot is fp64")
+    if ub is None:
+        ub = lb + x.numel() - 1
+    g = default_grid(dev)
+    teams = teams or g.teams
+    threads = threads or g.threads
+    m = _code(_lib.MODE_NAMES, mode)
+    if out is None:
+        out = torch.zeros(1, dtype=torch.float64, device=dev)
+    ws = reduce_workspace(dev, teams, threads, m)
+    check(_lib.load().omprt_dot(_p(x), _p(y), lb, ub, _code(_lib.SCHED_NAMES, sched), chunk,
+                                teams, threads, m, _p(ws), _p(out), _stream(x)), "omprt_dot")
+    return out
+
+
+def combine_partials(partials: torch.Tensor, op="add", out: torch.Tensor | None = None) -> torch.Tensor:
+    """out = out OP p[0] OP p[1] ... in order (multi-GPU combine tail)."""
+    dev = _dev(partials)
+    if out is None:
+        out = torch.zeros(1, dtype=partials.dtype, device=dev)
+    check(_lib.load().omprt_combine_partials(_p(partials), partials.numel(),
+                                             dtype_code(partials.dtype),
+                                             _code(_lib.OP_NAMES, op), _p(out),
+                                             _stream(partials)), "omprt_combine_partials")
+    return out
+
+
+# -------------------------------------------------------------- generic
+
+def generic_reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = None,
+                   teams: int = 1024, par_threads: int = 256, ordered: bool = False,
+                   pad_bytes: int = 0, heap_fallback: bool = False,
+                   heap_bytes_per_team: int = 1 << 20, out: torch.Tensor | None = None,
+                   team_offsets: torch.Tensor | None = None) -> torch.Tensor:
+    """Generic-mode region with __kmpc_alloc_shared globalisation and a nested
+    parallel reduce (config 4).  Does not synchronise; call check_trap()."""
+    dev = _dev(x)
+    if ub is None:
+        ub = lb + x.numel() - 1
+    if out is None:
+        out = torch.zeros(1, dtype=x.dtype, device=dev)
+    L = _lib.load()
+    nb = L.omprt_generic_workspace_bytes(teams, par_threads, int(heap_fallback),
+                                         heap_bytes_per_team)
+    ws = workspace(dev, nb)
+    check(L.omprt_generic_reduce(_p(x), lb, ub, dtype_code(x.dtype), _code(_lib.OP_NAMES, op),
+                                 teams, par_threads, int(ordered), pad_bytes, int(heap_fallback),
+                                 heap_bytes_per_team, _p(ws), _p(out), _p(team_offsets),
+                                 _stream(x)), "omprt_generic_reduce")
+    return out
+
+
+# -------------------------------------------------------- arena / atomics
+
+def arena_replay(script, *, teams: int = 1, threads: int = 32, caller_tid: int = 0,
+                 capacity: int = _lib.ARENA_CAPACITY, heap_fallback: bool = False,
+                 heap_bytes_per_team: int = 0, device="cuda") -> tuple[torch.Tensor, DeviceTrap | None]:
+    """Run an alloc/free script ([(op, bytes, offset), ...]) on every team's
+    device arena.  Returns (results [teams, nops] int64, trap or None)."""
+    s = torch.as_tensor(script, dtype=torch.int64).reshape(-1, 3).to(device)
+    dev = _dev(s)
+    nops = s.shape[0]
+    res = torch.zeros((teams, max(nops, 1)), dtype=torch.int64, device=dev)
+    heap = None
+    if heap_fallback:
+        heap = torch.zeros(max(teams * heap_bytes_per_team, 16), dtype=torch.uint8, device=dev)
+    st = _lib.load().omprt_arena_replay(_p(s), nops, teams, threads, caller_tid, capacity,
+                                        int(heap_fallback), heap_bytes_per_team, _p(heap),
+                                        _p(res), _stream(s))
+    check(st, "omprt_arena_replay")
+    trap = check_trap(dev) if st == _lib.TRAP else None
+    return res[:, :nops], trap
+
+
+def atomic_probe(kind: int, dtype, operands, desired=None, *, teams: int, threads: int,
+                 init: int = 0, device="cuda") -> tuple[int, list[int]]:
+    """Every thread g applies one seq_cst RMW with operands[g] to one cell.
+    Returns (final cell, olds) as zero-extended words."""
+    dt = dtype_code(dtype)
+    n = teams * threads
+    ops = torch.tensor([v & (2**64 - 1) for v in operands], dtype=torch.uint64, device=device)
+    dev = _dev(ops)
+    des = None
+    if desired is not None:
+        des = torch.tensor([v & (2**64 - 1) for v in desired], dtype=torch.uint64, device=dev)
+    bits = 32 if dt in (_lib.I32, _lib.U32) else 64
+    cell = torch.tensor([init & (2**bits - 1)], dtype=torch.uint32 if bits == 32 else torch.uint64,
+                        device=dev)
+    old = torch.zeros(n, dtype=torch.uint64, device=dev)
+    check(_lib.load().omprt_atomic_probe(kind, dt, _p(ops), _p(des), _p(cell), _p(old), teams,
+                                         threads, _stream(ops)), "omprt_atomic_probe")
+    return int(cell.cpu().item()), [int(v) for v in old.cpu().tolist()]
+
+
+def atomic_apply(kind: int, dtype, cells, operands, desired=None,
+                 device="cuda") -> tuple[list[int], list[int]]:
+    """Batched step semantics: returns (new cells, olds) as zero-extended words."""
+    dt = dtype_code(dtype)
+    bits = 32 if dt in (_lib.I32, _lib.U32) else 64
+    m = 2**bits - 1
+    ct = torch.tensor([v & m for v in cells], dtype=torch.uint32 if bits == 32 else torch.uint64,
+                      device=device)
+    dev = _dev(ct)
+    ops = torch.tensor([v & (2**64 - 1) for v in operands], dtype=torch.uint64, device=dev)
+    des = None
+    if desired is not None:
+        des = torch.tensor([v & (2**64 - 1) for v in desired], dtype=torch.uint64, device=dev)
+    old = torch.zeros(len(cells), dtype=torch.uint64, device=dev)
+    check(_lib.load().omprt_atomic_apply(kind, dt, _p(ct), _p(ops), _p(des), _p(old), len(cells),
+                                         _stream(ct)), "omprt_atomic_apply")
+    return [int(v) for v in ct.cpu().tolist()], [int(v) for v in old.cpu().tolist()]
+
+
+# ------------------------------------------------------------------ data
+
+def fill(x: torch.Tensor, seed: int, k: int = 0, offset: int = 0) -> torch.Tensor:
+    """Counter-based synthetic data in place (see omprt_fill)."""
+    _dev(x)
+    check(_lib.load().omprt_fill(_p(x), x.numel(), dtype_code(x.dtype), seed, k, offset,
+                                 _stream(x)), "omprt_fill")
+    return x
+
+
+def synthetic(n: int, dtype, seed: int, k: int = 0, offset: int = 0, device="cuda") -> torch.Tensor:
+    x = torch.empty(n, dtype=torch_dtype(dtype_code(dtype)), device=device)
+    return fill(x, seed, k, offset)

@@ -1,0 +1,62 @@
+"""Shared test helpers (test infrastructure)."""
+
+from __future__ import annotations
+
+from functools import lru_cache
+
+from oracle import oracle as O
+
+KIND = {"add": O.A_ADD, "max": O.A_MAX, "min": O.A_MIN, "xchg": O.A_XCHG, "cas": O.A_CAS,
+        "inc": O.A_INC}
+DT = {"i32": O.I32, "u32": O.U32, "i64": O.I64, "u64": O.U64}
+OPS = {"add": O.ADD, "max": O.MAX, "min": O.MIN}
+
+
+def linearizable(kind: int, dtype: int, init: int, ops, desired, olds, final) -> bool:
+    """Is there an order of the single-RMW threads whose replay through the
+    oracle's step semantics yields exactly the observed old values and final
+    cell?  (SPEC acceptance criterion 5; brute force with memoisation over the
+    set of threads already placed.)"""
+    n = len(ops)
+    ops = list(ops)
+    desired = list(desired) if desired is not None else [0] * n
+    olds = list(olds)
+
+    @lru_cache(maxsize=None)
+    def search(done: int, cell: int) -> bool:
+        if done == (1 << n) - 1:
+            return cell == final
+        tried = set()
+        for g in range(n):
+            if done >> g & 1 or olds[g] != cell:
+                continue
+            key = (ops[g], desired[g])
+            if key in tried:  # identical pending ops are interchangeable
+                continue
+            tried.add(key)
+            new, _ = O.atomic_step(kind, dtype, cell, ops[g], desired[g])
+            if search(done | (1 << g), new):
+                return True
+        return False
+
+    return search(0, init)
+
+
+def fold_int(op: str, bits: int, signed: bool, init: int, vals) -> int:
+    """Python restatement of the integer combine (wrap / signed compare)."""
+    m = (1 << bits) - 1
+
+    def sv(v):
+        v &= m
+        return v - (1 << bits) if signed and v >> (bits - 1) else v
+
+    acc = sv(init)
+    for v in vals:
+        v = sv(v)
+        if op == "add":
+            acc = sv(acc + v)
+        elif op == "max":
+            acc = v if acc < v else acc
+        else:
+            acc = v if acc > v else acc
+    return acc
