@@ -120,8 +120,15 @@ const char *omprt_last_error(void);
 int omprt_device_init(int device);
 
 /* Tuning knob (not part of the reference interface): 16-byte vectors each
- * lane keeps in flight per loop iteration in the SPMD loops (2, 4 or 8). */
+ * lane keeps in flight per loop iteration in the LDG-fed SPMD loops (2, 4 or
+ * 8).  4 (the default) lets contiguous-schedule reductions use the TMA
+ * bulk-copy path; 2 or 8 force the LDG path. */
 int omprt_set_unroll(int unroll);
+
+/* Tuning knob (not part of the reference interface): kernel variant used by
+ * the fp64 sum in SPMD mode — 0 default; 1-5 LDG load-policy / unroll
+ * variants; 10-16 TMA bulk-copy (cp.async.bulk + mbarrier) stage rings. */
+int omprt_set_variant(int variant);
 
 /* Number of streaming multiprocessors of the current device (148 on B200). */
 int omprt_num_sms(void);

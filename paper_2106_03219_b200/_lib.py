@@ -57,6 +57,7 @@ _SIGS = {
     "omprt_last_error": ([], C.c_char_p),
     "omprt_device_init": ([C.c_int], C.c_int),
     "omprt_set_unroll": ([C.c_int], C.c_int),
+    "omprt_set_variant": ([C.c_int], C.c_int),
     "omprt_num_sms": ([], C.c_int),
     "omprt_check_trap": ([C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                           C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),

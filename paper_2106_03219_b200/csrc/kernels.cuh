@@ -96,32 +96,46 @@ template <class T> OMPRT_D uint4 pack(const T (&in)[16 / sizeof(T)]) {
 }
 
 // part = part OP x[i] — the PARTIAL_SUMS loop body (corpus.py:219-247).
-template <class T, int OP> struct ReduceBody {
-  static constexpr int V = 16 / sizeof(T);
+// VB = bytes per lane per load (16: LDG.128, 32: LDG.256 on sm_100).
+template <class T, int OP, int LP = kLoadDefault, int VB = 16> struct ReduceBody {
+  static constexpr int V = VB / sizeof(T);
+  static constexpr int V16 = 16 / sizeof(T);
   const T *__restrict__ x;
-  T acc[V];
+  T acc[V16];
   OMPRT_D explicit ReduceBody(const T *x_) : x(x_) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) acc[j] = Red<OP, T>::identity();
+    for (int j = 0; j < V16; ++j) acc[j] = Red<OP, T>::identity();
   }
-  OMPRT_D bool head_ok(int64_t i) const { return (((uintptr_t)(x + i)) & 15) == 0; }
+  OMPRT_D bool head_ok(int64_t i) const { return (((uintptr_t)(x + i)) & (VB - 1)) == 0; }
   OMPRT_D void scalar(int64_t i) { acc[0] = Red<OP, T>::apply(acc[0], x[i]); }
   template <int U> OMPRT_D void vecs(const int64_t (&e)[U]) {
-    uint4 r[U];
+    if constexpr (VB == 32) {
+      U8x32 r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = ld_stream_v4(x + e[u]);
+      for (int u = 0; u < U; ++u) r[u] = ld_v8<LP>(x + e[u]);
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      T t[V];
-      unpack<T>(r[u], t);
+      for (int u = 0; u < U; ++u) {
+        consume(r[u].lo);
+        consume(r[u].hi);
+      }
+    } else {
+      uint4 r[U];
 #pragma unroll
-      for (int j = 0; j < V; ++j) acc[j] = Red<OP, T>::apply(acc[j], t[j]);
+      for (int u = 0; u < U; ++u) r[u] = ld_v4<LP>(x + e[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) consume(r[u]);
     }
+  }
+  OMPRT_D void consume(const uint4 &r) {
+    T t[V16];
+    unpack<T>(r, t);
+#pragma unroll
+    for (int j = 0; j < V16; ++j) acc[j] = Red<OP, T>::apply(acc[j], t[j]);
   }
   OMPRT_D T total() const {
     T v = acc[0];
 #pragma unroll
-    for (int j = 1; j < V; ++j) v = Red<OP, T>::apply(v, acc[j]);
+    for (int j = 1; j < V16; ++j) v = Red<OP, T>::apply(v, acc[j]);
     return v;
   }
 };
@@ -221,12 +235,12 @@ struct LoopArgs {
   int sched;
 };
 
-template <class T, int OP, int U>
+template <class T, int OP, int U, int LP = kLoadDefault, int VB = 16>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
   __shared__ T scratch[32];
   const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
-  ReduceBody<T, OP> body(x);
+  ReduceBody<T, OP, LP, VB> body(x);
   run_team<U>(body, s, threadIdx.x, blockDim.x);
   const T team_val = block_reduce<OP, T>(body.total(), scratch, blockDim.x);
   T *partials = (T *)ws.team_partials;

@@ -238,6 +238,61 @@ OMPRT_D uint4 ld_stream_v4(const void *p) {
   return r;
 }
 
+// Load-policy variants of the streaming load (tuning; kLoadDefault is what
+// every kernel uses unless a tuned variant is selected).
+enum LoadPolicy : int {
+  kLoadNcL2_256B = 0,  // ld.global.nc.L1::no_allocate.L2::256B
+  kLoadNc = 1,         // ld.global.nc.L1::no_allocate
+  kLoadEvictFirst = 2, // ld.global.nc.L1::no_allocate.L2::evict_first
+  kLoadPlain = 3,      // ld.global.nc (LDG.CONSTANT, L1 allocating)
+  kLoadDefault = kLoadNcL2_256B
+};
+
+template <int LP> OMPRT_D uint4 ld_v4(const void *p) {
+  uint4 r;
+  if constexpr (LP == kLoadNcL2_256B) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  } else if constexpr (LP == kLoadNc) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  }
+  return r;
+}
+
+// 256-bit loads (sm_100: LDG.E.256): 32 bytes per lane per instruction.
+struct U8x32 {
+  uint4 lo, hi;
+};
+
+template <int LP> OMPRT_D U8x32 ld_v8(const void *p) {
+  U8x32 r;
+  if constexpr (LP == kLoadNcL2_256B) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x),
+                   "=r"(r.hi.y), "=r"(r.hi.z), "=r"(r.hi.w)
+                 : "l"(p));
+  } else if constexpr (LP == kLoadEvictFirst) {
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x), "=r"(r.hi.y),
+          "=r"(r.hi.z), "=r"(r.hi.w)
+        : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.lo.x), "=r"(r.lo.y), "=r"(r.lo.z), "=r"(r.lo.w), "=r"(r.hi.x),
+                   "=r"(r.hi.y), "=r"(r.hi.z), "=r"(r.hi.w)
+                 : "l"(p));
+  }
+  return r;
+}
+
 // 128-bit load of data that this kernel also writes (y in axpy): coherent path.
 OMPRT_D uint4 ld_rw_v4(const void *p) {
   uint4 r;

@@ -9,6 +9,7 @@
 #include <string>
 #include <type_traits>
 
+#include "bulk.cuh"
 #include "generic.cuh"
 
 using namespace omprt;
@@ -41,7 +42,8 @@ int check_launch(const char *what) {
 
 inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-int g_unroll = 4;  // tuning knob: vectors in flight per lane per iteration
+int g_unroll = 4;   // tuning knob: vectors in flight per lane per iteration
+int g_variant = 0;  // tuning knob: kernel variant of the fp64 sum (0 = default)
 
 int check_grid(int teams, int threads) {
   if (teams < 1) return fail(OMPRT_EINVAL, "teams must be >= 1 (got %d)", teams);
@@ -61,13 +63,70 @@ int check_sched(int sched, int64_t chunk) {
 
 // ---------------------------------------------------------------- dispatch
 
+template <class K> int set_smem(K kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return OMPRT_OK;
+  cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return fail(OMPRT_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+  return OMPRT_OK;
+}
+
+template <class T, int OP, int STAGES, int SB>
+int launch_bulk(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
+                cudaStream_t st) {
+  auto kern = k_reduce_bulk<T, OP, STAGES, SB>;
+  const size_t smem = BulkSmem<STAGES, SB>::bytes;
+  int rc = set_smem(kern, smem);
+  if (rc) return rc;
+  kern<<<teams, threads, smem, st>>>(xp, la, w, op);
+  return check_launch("omprt_reduce(bulk)");
+}
+
+// Tuning variants of the fp64 sum (selected by omprt_set_variant).
+template <class T, int OP>
+int launch_variant(int v, const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
+                   cudaStream_t st) {
+  const bool contiguous = la.sched != OMPRT_SCHED_STATIC_CHUNKED;
+  const bool bulk_ok = contiguous && threads >= 64 && threads % 32 == 0;
+  switch (v) {
+    case 1: k_reduce<T, OP, 4, kLoadNc><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 2: k_reduce<T, OP, 4, kLoadEvictFirst, 32><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 3: k_reduce<T, OP, 4, kLoadPlain><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 4: k_reduce<T, OP, 8, kLoadNc><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 5: k_reduce<T, OP, 2, kLoadNcL2_256B, 32><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 6: k_reduce<T, OP, 4, kLoadNcL2_256B, 32><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 7: k_reduce<T, OP, 4, kLoadNc, 32><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 8: k_reduce<T, OP, 2, kLoadNc, 32><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 9: k_reduce<T, OP, 2, kLoadEvictFirst, 32><<<teams, threads, 0, st>>>(xp, la, w, op); break;
+    case 10: if (bulk_ok) return launch_bulk<T, OP, 4, 16384>(xp, la, teams, threads, w, op, st); break;
+    case 11: if (bulk_ok) return launch_bulk<T, OP, 8, 16384>(xp, la, teams, threads, w, op, st); break;
+    case 12: if (bulk_ok) return launch_bulk<T, OP, 4, 32768>(xp, la, teams, threads, w, op, st); break;
+    case 13: if (bulk_ok) return launch_bulk<T, OP, 3, 32768>(xp, la, teams, threads, w, op, st); break;
+    case 14: if (bulk_ok) return launch_bulk<T, OP, 6, 16384>(xp, la, teams, threads, w, op, st); break;
+    case 15: if (bulk_ok) return launch_bulk<T, OP, 2, 32768>(xp, la, teams, threads, w, op, st); break;
+    case 16: if (bulk_ok) return launch_bulk<T, OP, 12, 8192>(xp, la, teams, threads, w, op, st); break;
+    default: return fail(OMPRT_EINVAL, "unknown variant %d", v);
+  }
+  if (v >= 10) k_reduce<T, OP, 4><<<teams, threads, 0, st>>>(xp, la, w, op);
+  return check_launch("omprt_reduce(variant)");
+}
+
 template <class T, int OP>
 int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode, Workspace w,
                     void *out, cudaStream_t st) {
   const T *xp = (const T *)x;
   T *op = (T *)out;
+  if constexpr (std::is_same<T, double>::value && OP == OMPRT_OP_ADD) {
+    if (g_variant != 0 && mode == OMPRT_MODE_SPMD)
+      return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
+  }
+  const bool bulk_ok = la.sched != OMPRT_SCHED_STATIC_CHUNKED && threads >= 64 &&
+                       threads % 32 == 0 && g_unroll == 4;
   if (mode == OMPRT_MODE_ORDERED) {
     k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
+  } else if (bulk_ok) {
+    // default SPMD path for contiguous team sets: TMA bulk-copy stage ring
+    return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, threads, w, op, st);
   } else if (g_unroll >= 8) {
     k_reduce<T, OP, 8><<<teams, threads, 0, st>>>(xp, la, w, op);
   } else if (g_unroll <= 2) {
@@ -278,6 +337,12 @@ int omprt_set_unroll(int unroll) {
   if (unroll != 2 && unroll != 4 && unroll != 8)
     return fail(OMPRT_EINVAL, "unroll must be 2, 4 or 8 (got %d)", unroll);
   g_unroll = unroll;
+  return OMPRT_OK;
+}
+
+int omprt_set_variant(int variant) {
+  if (variant < 0) return fail(OMPRT_EINVAL, "variant must be >= 0");
+  g_variant = variant;
   return OMPRT_OK;
 }
 

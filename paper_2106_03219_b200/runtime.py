@@ -72,6 +72,11 @@ def set_unroll(unroll: int) -> None:
     check(_lib.load().omprt_set_unroll(unroll), "omprt_set_unroll")
 
 
+def set_variant(variant: int) -> None:
+    """Tuning: kernel variant of the fp64 sum (see omprt_set_variant)."""
+    check(_lib.load().omprt_set_variant(variant), "omprt_set_variant")
+
+
 @dataclass(frozen=True)
 class Grid:
     """Launch geometry: num_teams x thread_limit (GridConfig, vgpu.py:50-61)."""
@@ -80,9 +85,10 @@ class Grid:
     threads: int
 
 
-def default_grid(device: torch.device | None = None, threads: int = 1024,
-                 teams_per_sm: int = 2) -> Grid:
-    """A persistent grid: teams_per_sm resident teams on every SM."""
+def default_grid(device: torch.device | None = None, threads: int = 256,
+                 teams_per_sm: int = 1) -> Grid:
+    """A persistent grid: teams_per_sm resident teams on every SM (one
+    256-thread team per SM holds the 128 KiB bulk-copy ring)."""
     if device is not None:
         _lib.ensure_device(device.index or 0)
     return Grid(num_sms() * teams_per_sm, threads)

@@ -1,0 +1,130 @@
+"""Summarise an ncu report (--set full) or a launch-list CSV into profiles/.
+
+    python tools/ncu_summary.py report gpurun_out/prof.ncu-rep profiles/<name>.json \
+        [--algorithmic-bytes B]
+    python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/<name>.json
+
+The report summary keeps the counters the design is judged on: DRAM bytes
+read/written per launch (traffic vs the algorithmic bytes), DRAM throughput,
+duration, occupancy/registers, warp-stall reasons, shared-memory bank
+conflicts, and the SASS evidence of TMA (UBLKCP) when present.
+"""
+
+from __future__ import annotations
+
+import csv
+import io
+import json
+import subprocess
+import sys
+from collections import defaultdict
+
+KEEP = (
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "dram__bytes.sum.per_second",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_sectors_srcunit_tex_op_read.sum",
+    "lts__t_bytes.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread",
+    "launch__grid_size",
+    "launch__block_size",
+    "launch__shared_mem_per_block_dynamic",
+    "launch__occupancy_limit_shared_mem",
+    "launch__occupancy_limit_registers",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+    "smsp__cycles_active.avg",
+    "sm__cycles_elapsed.avg.per_second",
+)
+
+BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+TIME = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3,
+        "second": 1.0, "s": 1.0}
+RATE = {"byte/s": 1, "Kbyte/s": 1e3, "Mbyte/s": 1e6, "Gbyte/s": 1e9, "Tbyte/s": 1e12}
+UNIT_SCALE = {**BYTES, **TIME}
+
+
+def _scaled(h: str, u: str, x: float) -> tuple[str, float]:
+    if u in BYTES:
+        return f"{h} [bytes]", x * BYTES[u]
+    if u in TIME:
+        return f"{h} [s]", x * TIME[u]
+    if u in RATE:
+        return f"{h} [bytes/s]", x * RATE[u]
+    return h, x
+
+
+def _num(v: str) -> float | None:
+    try:
+        return float(v.replace(",", ""))
+    except ValueError:
+        return None
+
+
+def report(path: str, out: str, algorithmic: float | None) -> dict:
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    launches = []
+    for vals in rows[2:]:
+        rec = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else None}
+        stalls = {}
+        for h, u, v in zip(hdr, units, vals):
+            x = _num(v)
+            if h in KEEP and x is not None:
+                key, val = _scaled(h, u, x)
+                rec[key] = val
+            if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith(
+                    "_per_issue_active.ratio") and x is not None:
+                stalls[h[len("smsp__average_warps_issue_stalled_"):-len(
+                    "_per_issue_active.ratio")]] = x
+        rec["stall_reasons_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:8])
+        rd = rec.get("dram__bytes_read.sum [bytes]")
+        wr = rec.get("dram__bytes_write.sum [bytes]")
+        if rd is not None and wr is not None:
+            rec["dram_bytes_per_launch"] = rd + wr
+            if algorithmic:
+                rec["algorithmic_bytes_per_launch"] = algorithmic
+                rec["traffic_over_algorithmic"] = (rd + wr) / algorithmic
+        launches.append(rec)
+    res = {"source": path, "launches": launches}
+    if launches:
+        res["dram_bytes_per_launch"] = launches[0].get("dram_bytes_per_launch")
+    with open(out, "w") as f:
+        json.dump(res, f, indent=1)
+    return res
+
+
+def launches(path: str, out: str) -> dict:
+    rows = list(csv.reader(open(path)))
+    i = next(k for k, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[i]
+    agg = defaultdict(list)
+    for r in rows[i + 1:]:
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        scale = UNIT_SCALE.get(d.get("Metric Unit", "nsecond"), 1e-9)
+        agg[d["Kernel Name"].split("(")[0]].append(float(d["Metric Value"].replace(",", "")) * scale)
+    total = sum(sum(v) for v in agg.values())
+    res = {"source": path, "total_seconds": total, "kernels": [
+        {"kernel": k, "launches": len(v), "avg_us": sum(v) / len(v) * 1e6,
+         "share_of_time": sum(v) / total} for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1]))]}
+    with open(out, "w") as f:
+        json.dump(res, f, indent=1)
+    return res
+
+
+if __name__ == "__main__":
+    mode, src, dst = sys.argv[1:4]
+    alg = None
+    if "--algorithmic-bytes" in sys.argv:
+        alg = float(sys.argv[sys.argv.index("--algorithmic-bytes") + 1])
+    r = report(src, dst, alg) if mode == "report" else launches(src, dst)
+    print(json.dumps(r, indent=1)[:3000])
