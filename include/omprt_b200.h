@@ -242,7 +242,8 @@ int omprt_generic_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int
  * offset for an alloc, 0 for a free, -code at the trapping op (later ops -0x7fff).
  * After each alloc every thread of the team writes and re-reads a tag pattern
  * through the returned offset (data-path check; mismatch -> trap Abort).
- * Returns OMPRT_TRAP if any team trapped (synchronises), else OMPRT_OK. */
+ * Synchronises; returns OMPRT_TRAP if any team trapped (the trap word is
+ * left set for omprt_check_trap), else OMPRT_OK. */
 int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads,
                        int caller_tid, int64_t capacity, int heap_fallback,
                        int64_t heap_bytes_per_team, void *d_heap, int64_t *d_results,

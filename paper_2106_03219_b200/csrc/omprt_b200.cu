@@ -495,8 +495,11 @@ int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads
                                     (int)smem));
   k_arena_replay<<<teams, threads, smem, S(stream)>>>(d_script, nops, caller_tid, cfg, d_results);
   if ((rc = check_launch("omprt_arena_replay"))) return rc;
-  int kind = 0;
-  return omprt_check_trap(stream, &kind, nullptr, nullptr, nullptr);
+  // report (but leave) the trap word: omprt_check_trap reads and clears it
+  OMPRT_CUDA(cudaStreamSynchronize(S(stream)));
+  TrapWord t;
+  OMPRT_CUDA(cudaMemcpyFromSymbol(&t, g_trap, sizeof(t)));
+  return t.kind ? OMPRT_TRAP : OMPRT_OK;
 }
 
 int omprt_atomic_probe(int kind, int dtype, const uint64_t *d_operands, const uint64_t *d_desired,

@@ -1,0 +1,98 @@
+"""Config 3 (chunked static axpy + fp32 max/min) and config 5 (fp64 dot), GPU.
+
+axpy: y is elementwise bit-exact against the CPU restatement (both use one
+correctly rounded fused multiply-add, fmaf / __fmaf_rn), max/min bit-exact
+(order-independent, no NaN/-0 in the inputs).  dot: rel 1e-6 of the
+accurate sum in SPMD mode; bit-identical in ORDERED mode.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2106_03219_b200 import runtime
+
+pytestmark = pytest.mark.gpu
+
+SCHEDS = {"static": O.STATIC, "static_chunked": O.STATIC_CHUNKED,
+          "distribute": O.DISTRIBUTE, "distribute_chunked": O.DISTRIBUTE_CHUNKED}
+
+
+def axpy_case(cuda, n, a, sched, chunk, teams, threads, lb, ub, mode="spmd"):
+    x = O.fill(n, O.F32, O.SEED, 0)
+    y = O.fill(n, O.F32, O.SEED, 1)
+    yo = y.copy()
+    mx, mn = O.axpy_minmax(a, x, yo, lb, ub, SCHEDS[sched], chunk, teams, threads, -np.inf, np.inf)
+    xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+    gmx, gmn = runtime.axpy_minmax(a, xd, yd, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                                   threads=threads, mode=mode)
+    assert np.array_equal(yd.cpu().numpy(), yo), (sched, chunk, teams, threads, lb, ub)
+    assert float(gmx.item()) == mx and float(gmn.item()) == mn
+
+
+@pytest.mark.parametrize("chunk", [1, 64, 4096])
+@pytest.mark.parametrize("sched", ["static_chunked", "distribute_chunked"])
+@pytest.mark.parametrize("mode", ["spmd", "ordered"])
+def test_axpy_chunked_schedules(cuda, chunk, sched, mode):
+    n = 300_007
+    for teams, threads, lb, ub in ((4, 128, 0, n - 1), (37, 256, 3, n - 5), (1, 96, 1, 9999),
+                                    (148, 1024, 0, n - 1)):
+        axpy_case(cuda, n, 2.5, sched, chunk, teams, threads, lb, ub, mode)
+
+
+def test_axpy_block_schedules_and_misalignment(cuda):
+    n = 70_001
+    for sched in ("static", "distribute"):
+        for lb in range(4):
+            axpy_case(cuda, n, -1.75, sched, 1, 7, 64, lb, n - 1 - lb)
+
+
+def test_axpy_config3_full_size(cuda):
+    # N = 2^28 fp32 (1 GiB per array), chunk = 1, 64, 4096
+    n = 1 << 28
+    xd = runtime.synthetic(n, "f32", O.SEED, 0, device=cuda)
+    x = xd.cpu().numpy()
+    y0 = O.fill(n, O.F32, O.SEED, 1)
+    for chunk in (1, 64, 4096):
+        yd = torch.from_numpy(y0).to(cuda)
+        yo = y0.copy()
+        mx, mn = O.axpy_minmax(2.5, x, yo, 0, n - 1, O.DISTRIBUTE_CHUNKED, chunk, 148, 1024,
+                               -np.inf, np.inf)
+        gmx, gmn = runtime.axpy_minmax(2.5, xd, yd, sched="distribute_chunked", chunk=chunk,
+                                       teams=148, threads=1024)
+        assert float(gmx.item()) == mx and float(gmn.item()) == mn
+        assert torch.equal(yd, torch.from_numpy(yo).to(cuda))
+        del yd
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("sched", list(SCHEDS))
+def test_dot_matches_oracle(cuda, sched):
+    n = 500_003
+    x, y = O.fill(n, O.F64, O.SEED, 0), O.fill(n, O.F64, O.SEED, 1)
+    xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+    for teams, threads, lb, ub, chunk in ((5, 64, 0, n - 1, 1), (148, 256, 1, n - 2, 64),
+                                          (1, 32, 3, 1000, 7)):
+        truth = O.accurate_dot_gen(lb, ub)
+        got = float(runtime.dot(xd, yd, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                                threads=threads).item())
+        assert abs(got - truth) <= 1e-6 * truth
+        want = O.dot(x, y, lb, ub, SCHEDS[sched], chunk, teams, threads)
+        got_o = float(runtime.dot(xd, yd, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                                  threads=threads, mode="ordered").item())
+        assert got_o == want  # reference order: bit-identical
+
+
+def test_dot_full_shard(cuda):
+    # one GPU's shard of config 5 at 2^30 (two 8 GiB arrays)
+    n = 1 << 30
+    x = runtime.synthetic(n, "f64", O.SEED, 0, device=cuda)
+    y = runtime.synthetic(n, "f64", O.SEED, 1, device=cuda)
+    got = float(runtime.dot(x, y).item())
+    truth = O.accurate_dot_gen(0, n - 1)
+    assert abs(got - truth) <= 1e-6 * truth
+    del x, y
+    torch.cuda.empty_cache()
