@@ -24,6 +24,17 @@ def linearizable(kind: int, dtype: int, init: int, ops, desired, olds, final) ->
 
     @lru_cache(maxsize=None)
     def search(done: int, cell: int) -> bool:
+        # ops that observed this value and leave it unchanged (failed CAS,
+        # non-raising max, xchg of the same value) can be placed right now
+        # without loss of generality: they do not change what others see
+        changed = True
+        while changed:
+            changed = False
+            for g in range(n):
+                if not done >> g & 1 and olds[g] == cell:
+                    if O.atomic_step(kind, dtype, cell, ops[g], desired[g])[0] == cell:
+                        done |= 1 << g
+                        changed = True
         if done == (1 << n) - 1:
             return cell == final
         tried = set()
