@@ -64,20 +64,109 @@ OMPRT_D void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
 // (profiles/r1_steady_bulk.jsonl).
 constexpr int kBulkStages = 4;
 constexpr int kBulkStageBytes = 32768;
+// Two-stream rings (dot, axpy): 4 stages x 2 streams x 16 KiB = 128 KiB.
+constexpr int kBulk2Stages = 4;
+constexpr int kBulk2StageBytes = 16384;
 
 template <int STAGES, int STAGE_BYTES> struct BulkSmem {
   static constexpr size_t bytes = (size_t)STAGES * STAGE_BYTES;
 };
 
-// Stream [base, base + nbytes) (16-byte aligned, nbytes % 16 == 0) through
-// the stage ring; `consume(const uint4&)` is called by the consumer threads
-// (all warps but warp 0) for every 16-byte vector exactly once.
-template <int STAGES, int STAGE_BYTES, class F>
-OMPRT_D void bulk_stream(const unsigned char *base, int64_t nbytes, unsigned char *stages,
-                         uint64_t *full, uint64_t *empty, F &&consume) {
+// The bytes a team streams, as teeth: `nteeth` runs of `tooth` bytes,
+// `stride` bytes apart, the last one `last` bytes long; all 16-byte aligned
+// multiples of 16 (relative to each stream's base pointer).  A contiguous team
+// block is one tooth.  Stages never straddle a tooth boundary: a tooth larger
+// than a stage is cut into stage-sized pieces (case A), smaller teeth are
+// packed `per` to a stage (case B), so every stage is a handful of bulk copies.
+template <int STAGE_BYTES> struct BulkPlan {
+  int64_t first = 0, tooth = 0, stride = 0, nteeth = 0, last = 0;
+  int64_t spt = 0;  // case A: stages per full tooth
+  int64_t per = 0;  // case B: teeth per stage
+
+  OMPRT_D void finish() {
+    if (nteeth > 0 && last == 0) {
+      --nteeth;
+      last = tooth;
+    }
+    if (tooth > STAGE_BYTES) {
+      spt = (tooth + STAGE_BYTES - 1) / STAGE_BYTES;
+    } else if (tooth > 0) {
+      per = STAGE_BYTES / tooth;
+    }
+  }
+  OMPRT_D int64_t nstages() const {
+    if (nteeth <= 0) return 0;
+    if (spt) return (nteeth - 1) * spt + (last + STAGE_BYTES - 1) / STAGE_BYTES;
+    return (nteeth + per - 1) / per;
+  }
+  OMPRT_D int64_t tooth_len(int64_t r) const { return r == nteeth - 1 ? last : tooth; }
+  // case A: stage k -> (tooth r, byte offset inside the tooth, bytes)
+  // case B: stage k -> teeth [k*per, min(k*per+per, nteeth))
+  OMPRT_D int64_t stage_bytes(int64_t k) const {
+    if (spt) {
+      const int64_t r = k / spt, c = k % spt;
+      const int64_t rem = tooth_len(r) - c * STAGE_BYTES;
+      return rem < STAGE_BYTES ? rem : STAGE_BYTES;
+    }
+    const int64_t r0 = k * per;
+    const int64_t r1 = (r0 + per < nteeth) ? r0 + per : nteeth;
+    return (r1 - r0 - 1) * tooth + tooth_len(r1 - 1);
+  }
+  // Where the vectors of stage k live (computed once per stage, so the
+  // per-vector position is 32-bit arithmetic): byte offset (relative to the
+  // stream base) of vector v = base + (v / vpt) * stride + (v % vpt) * 16.
+  struct Loc {
+    int64_t base;
+    int64_t stride;
+    uint32_t vpt;  // 0: the stage is one contiguous piece
+    OMPRT_D int64_t byte_of(uint32_t v) const {
+      if (vpt == 0) return base + (int64_t)v * 16;
+      return base + (int64_t)(v / vpt) * stride + (int64_t)(v % vpt) * 16;
+    }
+  };
+  OMPRT_D Loc loc(int64_t k) const {
+    Loc l;
+    if (spt) {
+      const int64_t r = k / spt, c = k % spt;
+      l.base = first + r * stride + c * STAGE_BYTES;
+      l.stride = 0;
+      l.vpt = 0;
+    } else {
+      l.base = first + k * per * stride;
+      l.stride = stride;
+      l.vpt = (uint32_t)(tooth >> 4);
+    }
+    return l;
+  }
+  // Issue the bulk copies of stage k; lane `lane` of the producer warp takes
+  // pieces lane, lane+32, ... (a packed stage holds up to STAGE_BYTES/512).
+  template <class Issue> OMPRT_D void issue(int64_t k, uint32_t lane, Issue &&copy) const {
+    if (spt) {
+      if (lane == 0) {
+        const int64_t r = k / spt, c = k % spt;
+        copy(first + r * stride + c * STAGE_BYTES, 0, stage_bytes(k));
+      }
+      return;
+    }
+    const int64_t r0 = k * per;
+    const int64_t r1 = (r0 + per < nteeth) ? r0 + per : nteeth;
+    for (int64_t r = r0 + lane; r < r1; r += 32)
+      copy(first + r * stride, (r - r0) * tooth, tooth_len(r));
+  }
+};
+
+// Stream NS byte streams (same plan, different base pointers) through the
+// stage ring (stage st of stream j lives at stages + (st*NS + j)*STAGE_BYTES).
+// `consume(loc, v, r[0..NS))` is called by the consumer threads (all warps
+// but warp 0) exactly once for every 16-byte vector v of every stage; `loc`
+// (BulkPlan::Loc) locates v in the streams.
+template <int NS, int STAGES, int STAGE_BYTES, class F>
+OMPRT_D void bulk_stream_n(const unsigned char *const (&base)[NS],
+                           const BulkPlan<STAGE_BYTES> &plan, unsigned char *stages,
+                           uint64_t *full, uint64_t *empty, F &&consume) {
   const uint32_t warp = warp_id(), lane = lane_id();
   const uint32_t nwarps = blockDim.x >> 5;
-  const int64_t nchunks = (nbytes + STAGE_BYTES - 1) / STAGE_BYTES;
+  const int64_t nst = plan.nstages();
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -87,28 +176,173 @@ OMPRT_D void bulk_stream(const unsigned char *base, int64_t nbytes, unsigned cha
   }
   __syncthreads();
   if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      for (int64_t k = 0; k < nchunks; ++k) {
-        const int st = (int)(k % STAGES);
-        if (k >= STAGES) mbar_wait(&empty[st], (uint32_t)((k / STAGES - 1) & 1));
-        const int64_t rem = nbytes - k * STAGE_BYTES;
-        const uint32_t b = (uint32_t)(rem < STAGE_BYTES ? rem : STAGE_BYTES);
-        mbar_expect_tx(&full[st], b);
-        bulk_g2s(stages + (size_t)st * STAGE_BYTES, base + k * STAGE_BYTES, b, &full[st], pol);
-      }
+    // producer warp: lane 0 arms the stage's transaction count, then the
+    // lanes issue its bulk copies in parallel
+    const uint64_t pol = policy_evict_first();
+    for (int64_t k = 0; k < nst; ++k) {
+      const int st = (int)(k % STAGES);
+      if (k >= STAGES) mbar_wait(&empty[st], (uint32_t)((k / STAGES - 1) & 1));
+      if (lane == 0) mbar_expect_tx(&full[st], (uint32_t)(plan.stage_bytes(k) * NS));
+      __syncwarp();
+      plan.issue(k, lane, [&](int64_t src, int64_t dst, int64_t bytes) {
+#pragma unroll
+        for (int j = 0; j < NS; ++j)
+          bulk_g2s(stages + ((size_t)st * NS + j) * STAGE_BYTES + dst, base[j] + src,
+                   (uint32_t)bytes, &full[st], pol);
+      });
     }
   } else {
     const uint32_t ct = threadIdx.x - 32, nc = blockDim.x - 32;
-    for (int64_t k = 0; k < nchunks; ++k) {
+    for (int64_t k = 0; k < nst; ++k) {
       const int st = (int)(k % STAGES);
       mbar_wait(&full[st], (uint32_t)((k / STAGES) & 1));
-      const int64_t rem = nbytes - k * STAGE_BYTES;
-      const uint32_t nvec = (uint32_t)((rem < STAGE_BYTES ? rem : STAGE_BYTES) >> 4);
-      const uint4 *sv = (const uint4 *)(stages + (size_t)st * STAGE_BYTES);
-      for (uint32_t v = ct; v < nvec; v += nc) consume(sv[v]);
+      const uint32_t nvec = (uint32_t)(plan.stage_bytes(k) >> 4);
+      const typename BulkPlan<STAGE_BYTES>::Loc where = plan.loc(k);
+      const uint4 *sv = (const uint4 *)(stages + (size_t)st * NS * STAGE_BYTES);
+      for (uint32_t v = ct; v < nvec; v += nc) {
+        uint4 r[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j) r[j] = sv[(size_t)j * (STAGE_BYTES / 16) + v];
+        consume(where, v, r);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+}
+
+// Split the team's iteration set into a bulk plan (16-byte aligned teeth for
+// every stream in `ptrs`) and the element-wise remainder walked by `scalar`:
+// an unaligned head (contiguous sets), the ragged end of the last tooth.
+// Returns false when the streams cannot be vectorised (mutually misaligned
+// or a comb whose teeth are not 16-byte multiples): the caller then walks
+// the set with per-lane loads instead.
+template <int STAGE_BYTES, int NP, class Scalar>
+OMPRT_D bool team_bulk_plan(const TeamSet &s, int elem, const void *const (&ptrs)[NP],
+                            BulkPlan<STAGE_BYTES> &plan, Scalar &&scalar) {
+  auto aligned = [&](int64_t i) {
+    uintptr_t a = 0;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) a |= (uintptr_t)ptrs[j] + (uintptr_t)(i * elem);
+    return (a & 15) == 0;
+  };
+  if (s.nseg <= 0) return true;
+  const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+  if (s.nseg == 1 || s.seg_stride == 0) {
+    int64_t count = s.ub - s.first + 1;
+    if (count > s.seg_len) count = s.seg_len;
+    const int V = 16 / elem;
+    int64_t head = 0;
+    while (head < V && head < count && !aligned(s.first + head)) ++head;
+    if (head < count && !aligned(s.first + head)) return false;
+    for (int64_t i = tid; i < head && i < count; i += nthr) scalar(s.first + i);
+    if (head >= count) return true;
+    const int64_t vb = ((count - head) * elem) & ~(int64_t)15;
+    plan.first = (s.first + head) * elem;
+    plan.tooth = plan.last = vb;
+    plan.nteeth = vb > 0 ? 1 : 0;
+    plan.stride = 0;
+    plan.finish();
+    for (int64_t i = head + vb / elem + tid; i < count; i += nthr) scalar(s.first + i);
+    return true;
+  }
+  // teeth below 512 bytes would cost one bulk copy per few vectors: the
+  // per-lane walker (run_comb) is the better engine there
+  if (!aligned(s.first) || (s.seg_len * elem) % 16 || (s.seg_stride * elem) % 16 ||
+      s.seg_len * elem < 512)
+    return false;
+  const int64_t last_first = s.first + (s.nseg - 1) * s.seg_stride;
+  int64_t last_len = s.ub - last_first + 1;
+  if (last_len > s.seg_len) last_len = s.seg_len;
+  plan.first = s.first * elem;
+  plan.tooth = s.seg_len * elem;
+  plan.stride = s.seg_stride * elem;
+  plan.nteeth = s.nseg;
+  plan.last = (last_len * elem) & ~(int64_t)15;
+  plan.finish();
+  for (int64_t i = (((last_len * elem) & ~(int64_t)15) / elem) + tid; i < last_len; i += nthr)
+    scalar(last_first + i);
+  return true;
+}
+
+// fp64 dot over the TMA ring: x and y chunks land in paired stages.
+template <int STAGES, int STAGE_BYTES, int U>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_dot_bulk(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
+               Workspace ws, double *out) {
+  extern __shared__ __align__(128) unsigned char stages[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ __align__(8) uint64_t empty[STAGES];
+  __shared__ double scratch[32];
+  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  DotBody body(x, y);
+  BulkPlan<STAGE_BYTES> plan;
+  const void *const ptrs[2] = {x, y};
+  if (team_bulk_plan<STAGE_BYTES>(s, 8, ptrs, plan, [&](int64_t i) { body.scalar(i); })) {
+    const unsigned char *const b[2] = {(const unsigned char *)x, (const unsigned char *)y};
+    bulk_stream_n<2, STAGES, STAGE_BYTES>(b, plan, stages, full, empty,
+                                          [&](const auto &, uint32_t, const uint4 (&r)[2]) {
+                                            double a[2], c[2];
+                                            unpack<double>(r[0], a);
+                                            unpack<double>(r[1], c);
+                                            body.acc[0] = __fma_rn(a[0], c[0], body.acc[0]);
+                                            body.acc[1] = __fma_rn(a[1], c[1], body.acc[1]);
+                                          });
+  } else {
+    run_team<U>(body, s, threadIdx.x, blockDim.x);
+  }
+  const double team_val = block_reduce<OMPRT_OP_ADD, double>(body.total(), scratch, blockDim.x);
+  double *partials = (double *)ws.team_partials;
+  if (teams_ticket<OMPRT_OP_ADD, double>(team_val, partials, ws.ticket)) {
+    const double v = combine_team_partials<OMPRT_OP_ADD, double>(partials, scratch);
+    if (threadIdx.x == 0) *out = *out + v;
+  }
+}
+
+// Chunked-schedule axpy + max/min over the TMA ring: x and y arrive by bulk
+// copy, the new y leaves by coalesced 16-byte stores.
+template <int STAGES, int STAGE_BYTES, int U>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_axpy_minmax_bulk(float a, const float *__restrict__ x, float *__restrict__ y, LoopArgs la,
+                       Workspace ws, float *out_max, float *out_min) {
+  extern __shared__ __align__(128) unsigned char stages[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ __align__(8) uint64_t empty[STAGES];
+  __shared__ float scratch[32];
+  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  AxpyBody body(a, x, y);
+  BulkPlan<STAGE_BYTES> plan;
+  const void *const ptrs[2] = {x, y};
+  if (team_bulk_plan<STAGE_BYTES>(s, 4, ptrs, plan, [&](int64_t i) { body.scalar(i); })) {
+    const unsigned char *const b[2] = {(const unsigned char *)x, (const unsigned char *)y};
+    unsigned char *yb = (unsigned char *)y;
+    bulk_stream_n<2, STAGES, STAGE_BYTES>(
+        b, plan, stages, full, empty, [&](const auto &where, uint32_t v, const uint4 (&r)[2]) {
+          float xv[4], yv[4];
+          unpack<float>(r[0], xv);
+          unpack<float>(r[1], yv);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            yv[j] = __fmaf_rn(a, xv[j], yv[j]);
+            body.mx[j] = Red<OMPRT_OP_MAX, float>::apply(body.mx[j], yv[j]);
+            body.mn[j] = Red<OMPRT_OP_MIN, float>::apply(body.mn[j], yv[j]);
+          }
+          st_stream_v4(yb + where.byte_of(v), pack<float>(yv));
+        });
+  } else {
+    run_team<U>(body, s, threadIdx.x, blockDim.x);
+  }
+  const float tmax = block_reduce<OMPRT_OP_MAX, float>(body.max_total(), scratch, blockDim.x);
+  const float tmin = block_reduce<OMPRT_OP_MIN, float>(body.min_total(), scratch, blockDim.x);
+  float *pmax = (float *)ws.team_partials;
+  float *pmin = pmax + gridDim.x;
+  if (threadIdx.x == 0) pmin[blockIdx.x] = tmin;
+  if (teams_ticket<OMPRT_OP_MAX, float>(tmax, pmax, ws.ticket)) {
+    const float vmax = combine_team_partials<OMPRT_OP_MAX, float>(pmax, scratch);
+    const float vmin = combine_team_partials<OMPRT_OP_MIN, float>(pmin, scratch);
+    if (threadIdx.x == 0) {
+      *out_max = Red<OMPRT_OP_MAX, float>::apply(*out_max, vmax);
+      *out_min = Red<OMPRT_OP_MIN, float>::apply(*out_min, vmin);
     }
   }
 }
@@ -121,22 +355,18 @@ __global__ void __launch_bounds__(kMaxThreads)
   __shared__ __align__(8) uint64_t empty[STAGES];
   __shared__ T scratch[32];
   const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
-  int64_t count = 0;
-  if (s.nseg > 0) {
-    count = s.ub - s.first + 1;
-    if (count > s.seg_len) count = s.seg_len;
-  }
   ReduceBody<T, OP> body(x);
-  constexpr int V = ReduceBody<T, OP>::V;
-  int64_t head = 0;
-  while (head < V && head < count && !body.head_ok(s.first + head)) ++head;
-  for (int64_t i = threadIdx.x; i < head; i += blockDim.x) body.scalar(s.first + i);
-  const int64_t nbytes = ((count - head) * (int64_t)sizeof(T)) & ~(int64_t)15;
-  if (nbytes > 0)
-    bulk_stream<STAGES, STAGE_BYTES>((const unsigned char *)(x + s.first + head), nbytes, stages,
-                                     full, empty, [&](const uint4 &r) { body.consume(r); });
-  const int64_t done = head + nbytes / (int64_t)sizeof(T);
-  for (int64_t i = done + threadIdx.x; i < count; i += blockDim.x) body.scalar(s.first + i);
+  BulkPlan<STAGE_BYTES> plan;
+  const void *const ptrs[1] = {x};
+  if (team_bulk_plan<STAGE_BYTES>(s, (int)sizeof(T), ptrs, plan,
+                                  [&](int64_t i) { body.scalar(i); })) {
+    const unsigned char *const b[1] = {(const unsigned char *)x};
+    bulk_stream_n<1, STAGES, STAGE_BYTES>(
+        b, plan, stages, full, empty,
+        [&](const auto &, uint32_t, const uint4 (&r)[1]) { body.consume(r[0]); });
+  } else {
+    run_team<4>(body, s, threadIdx.x, blockDim.x);
+  }
   const T team_val = block_reduce<OP, T>(body.total(), scratch, blockDim.x);
   T *partials = (T *)ws.team_partials;
   if (teams_ticket<OP, T>(team_val, partials, ws.ticket)) {

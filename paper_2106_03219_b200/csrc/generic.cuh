@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(kMaxThreads)
         for (int64_t i = mlb; i <= mub; ++i) part = Red<OP, T>::apply(part, x[i]);
         parts[wt] = part;
       } else {
-        ReduceBody<T, OP> body(x);
+        // 256-bit streaming loads: the worker warps share the SM with other
+        // teams, so each lane keeps U x 32 bytes in flight
+        ReduceBody<T, OP, kLoadNc, 32> body(x);
         if (tub >= tlb) run_contiguous<U>(body, tlb, tub - tlb + 1, wt, (uint32_t)P);
         // nested parallel reduce across the workers, scratch in the
         // globalised arena block, synchronised on the workers-only barrier

@@ -86,8 +86,7 @@ int launch_bulk(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T
 template <class T, int OP>
 int launch_variant(int v, const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
                    cudaStream_t st) {
-  const bool contiguous = la.sched != OMPRT_SCHED_STATIC_CHUNKED;
-  const bool bulk_ok = contiguous && threads >= 64 && threads % 32 == 0;
+  const bool bulk_ok = threads >= 64 && threads % 32 == 0;
   switch (v) {
     case 1: k_reduce<T, OP, 4, kLoadNc><<<teams, threads, 0, st>>>(xp, la, w, op); break;
     case 2: k_reduce<T, OP, 4, kLoadEvictFirst, 32><<<teams, threads, 0, st>>>(xp, la, w, op); break;
@@ -120,8 +119,7 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
     if (g_variant != 0 && mode == OMPRT_MODE_SPMD)
       return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
   }
-  const bool bulk_ok = la.sched != OMPRT_SCHED_STATIC_CHUNKED && threads >= 64 &&
-                       threads % 32 == 0 && g_unroll == 4;
+  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
   if (mode == OMPRT_MODE_ORDERED) {
     k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
   } else if (bulk_ok) {
@@ -254,7 +252,17 @@ int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, in
                      int64_t pad, ArenaCfg cfg, Workspace w, void *out, int64_t *offs,
                      cudaStream_t st) {
   auto kern = k_generic<T, OP, 4>;
-  const size_t smem = (size_t)cfg.capacity;
+  // Physical backing of the team arena: the region's known allocation
+  // footprint (pad, then parts[P+1]) capped at the semantic capacity.  The
+  // overflow check still uses cfg.capacity (64 KiB, the reference's
+  // ARENA_CAPACITY), so traps are unchanged; a small footprint just leaves
+  // room for more resident teams per SM.
+  const int64_t footprint =
+      (pad + 7) / 8 * 8 + (int64_t)(P + 1) * (int64_t)sizeof(T);
+  int64_t phys = footprint < cfg.capacity ? footprint : cfg.capacity;
+  phys = (phys + 15) / 16 * 16;
+  if (phys < 16) phys = 16;
+  const size_t smem = (size_t)phys;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -396,10 +404,17 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
     return fail(OMPRT_EINVAL, "axpy_minmax: null device pointer");
   LoopArgs la{lb, ub, chunk, sched};
   Workspace w = ws_carve(d_ws, teams, 2);
-  if (mode == OMPRT_MODE_ORDERED)
+  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
+  if (mode == OMPRT_MODE_ORDERED) {
     k_axpy_minmax_ordered<<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
-  else
+  } else if (bulk_ok) {
+    auto kern = k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
+    const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
+    if ((rc = set_smem(kern, smem))) return rc;
+    kern<<<teams, threads, smem, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+  } else {
     k_axpy_minmax<4><<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+  }
   return check_launch("omprt_axpy_minmax");
 }
 
@@ -412,9 +427,15 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
     return fail(OMPRT_EINVAL, "dot: null device pointer");
   LoopArgs la{lb, ub, chunk, sched};
   Workspace w = ws_carve(d_ws, teams, 2);
-  if (mode == OMPRT_MODE_ORDERED)
+  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
+  if (mode == OMPRT_MODE_ORDERED) {
     k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
-  else if (g_unroll >= 8)
+  } else if (bulk_ok) {
+    auto kern = k_dot_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
+    const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
+    if ((rc = set_smem(kern, smem))) return rc;
+    kern<<<teams, threads, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
+  } else if (g_unroll >= 8)
     k_dot<8><<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
   else
     k_dot<4><<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);

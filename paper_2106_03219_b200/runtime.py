@@ -147,9 +147,10 @@ _ws_cache: dict[tuple, torch.Tensor] = {}
 
 
 def workspace(device: torch.device, nbytes: int) -> torch.Tensor:
-    """Zeroed device workspace, cached per device (the last-team-finishes
-    ticket self-resets, so reuse across launches on one stream is safe)."""
-    key = (device.type, device.index or 0)
+    """Zeroed device workspace, cached per (device, stream): the
+    last-team-finishes ticket self-resets, so launches ordered on one stream
+    may share it; concurrent streams each get their own."""
+    key = (device.type, device.index or 0, torch.cuda.current_stream(device).cuda_stream)
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
