@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU")
+    p.add_argument("--backend", default="nccl",
+                   help="torch.distributed backend for N > 1 (gloo: debug the multi-rank "
+                        "flow with several ranks sharing one GPU)")
     return p.parse_args()
 
 
@@ -136,6 +139,8 @@ def cpu_reference(n_sample: int, steps: int, warmup: int, teams: int, threads: i
     fp64 array of n_sample elements."""
     from oracle import oracle as O
 
+    # every host core this process may run on (torchrun sets OMP_NUM_THREADS=1)
+    O.set_threads(len(os.sched_getaffinity(0)))
     x = O.fill(n_sample, O.F64, SEED, 0)
     for _ in range(warmup):
         O.reduce(x, 0, n_sample - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, teams, threads)
@@ -154,7 +159,7 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     n_sample = 1 << 25
-    teams = args.teams or 296
+    teams = args.teams or 148  # our arm's default geometry: one team per B200 SM
     r = cpu_reference(n_sample, args.steps, args.warmup, teams, args.threads)
     line = {
         "impl": "reference",
@@ -198,10 +203,14 @@ def run_ours(args) -> None:
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N > 1 must be launched with torchrun")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
     _lib.ensure_device(local)
     if args.unroll:
         runtime.set_unroll(args.unroll)
@@ -333,7 +342,7 @@ def run_ours(args) -> None:
             "config": {"workload": "C2 teams distribute parallel for fp64 sum reduction, SPMD",
                        "n_per_gpu": n, "n_global": G * n, "schedule": args.sched,
                        "teams": teams, "threads": threads, "mode": "spmd",
-                       "parallelism": f"dp{G} (static_bounds shards + NCCL all-reduce)",
+                       "parallelism": f"dp{G} (static_bounds shards + {args.backend.upper()} all-reduce)",
                        "l2": "input 8 GiB per GPU >> 126 MB L2; no flush needed",
                        "frac_of_hbm_peak": round(gbs / G / pk["hbm_gbs"], 4),
                        "frac_of_nominal_8tbs": round(gbs / G / 8000.0, 4)},
