@@ -160,7 +160,11 @@ template <int STAGE_BYTES> struct BulkPlan {
 // `consume(loc, v, r[0..NS))` is called by the consumer threads (all warps
 // but warp 0) exactly once for every 16-byte vector v of every stage; `loc`
 // (BulkPlan::Loc) locates v in the streams.
-template <int NS, int STAGES, int STAGE_BYTES, class F>
+// The consumers release a stage with an mbarrier arrive only (the
+// producer's wait on that mbarrier orders the stage's reads before the next
+// bulk copy into it — the CUTLASS TMA-pipeline consumer_release pattern);
+// PROXY_FENCE adds a fence.proxy.async per stage (tuning variant 17).
+template <int NS, int STAGES, int STAGE_BYTES, class F, bool PROXY_FENCE = false>
 OMPRT_D void bulk_stream_n(const unsigned char *const (&base)[NS],
                            const BulkPlan<STAGE_BYTES> &plan, unsigned char *stages,
                            uint64_t *full, uint64_t *empty, F &&consume) {
@@ -205,6 +209,8 @@ OMPRT_D void bulk_stream_n(const unsigned char *const (&base)[NS],
         for (int j = 0; j < NS; ++j) r[j] = sv[(size_t)j * (STAGE_BYTES / 16) + v];
         consume(where, v, r);
       }
+      if constexpr (PROXY_FENCE)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   }
 }
 
-template <class T, int OP, int STAGES, int STAGE_BYTES>
+template <class T, int OP, int STAGES, int STAGE_BYTES, bool PROXY_FENCE = false>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce_bulk(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
   extern __shared__ __align__(128) unsigned char stages[];
@@ -361,9 +367,9 @@ __global__ void __launch_bounds__(kMaxThreads)
   if (team_bulk_plan<STAGE_BYTES>(s, (int)sizeof(T), ptrs, plan,
                                   [&](int64_t i) { body.scalar(i); })) {
     const unsigned char *const b[1] = {(const unsigned char *)x};
-    bulk_stream_n<1, STAGES, STAGE_BYTES>(
-        b, plan, stages, full, empty,
-        [&](const auto &, uint32_t, const uint4 (&r)[1]) { body.consume(r[0]); });
+    auto consume = [&](const auto &, uint32_t, const uint4 (&r)[1]) { body.consume(r[0]); };
+    bulk_stream_n<1, STAGES, STAGE_BYTES, decltype(consume) &, PROXY_FENCE>(b, plan, stages, full,
+                                                                           empty, consume);
   } else {
     run_team<4>(body, s, threadIdx.x, blockDim.x);
   }

@@ -117,6 +117,7 @@ __global__ void k_arena_replay(const int64_t *__restrict__ script, int nops, int
     }
     __syncthreads();
     const int64_t r = s_res;
+    __syncthreads();  // every thread has read s_res before the next op rewrites it
     if (threadIdx.x == 0) res[op] = r;
     if (r < 0) {
       if (threadIdx.x == 0)

@@ -326,13 +326,14 @@ OMPRT_D void fence_acq_rel_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory
 // __kmpc_barrier / __kmpc_impl_syncthreads: barrier 0 over the whole team.
 OMPRT_D void kmpc_barrier() { __syncthreads(); }
 
-// Named barriers (bar.sync id, n / bar.arrive id, n): n counts threads and
-// must be a multiple of the warp size; every warp executes them convergently.
+// Named barriers: barrier.sync / barrier.arrive id, n (the non-.aligned
+// forms: each thread arrives on its own, so a warp need not be converged);
+// n counts threads and is a multiple of the warp size here.
 OMPRT_D void named_barrier_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 OMPRT_D void named_barrier_arrive(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // atomic_inc (runtime.mc:175-186; step_inc devicert.py:105-107):

@@ -71,10 +71,10 @@ template <class K> int set_smem(K kern, size_t bytes) {
   return OMPRT_OK;
 }
 
-template <class T, int OP, int STAGES, int SB>
+template <class T, int OP, int STAGES, int SB, bool FENCE = false>
 int launch_bulk(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
                 cudaStream_t st) {
-  auto kern = k_reduce_bulk<T, OP, STAGES, SB>;
+  auto kern = k_reduce_bulk<T, OP, STAGES, SB, FENCE>;
   const size_t smem = BulkSmem<STAGES, SB>::bytes;
   int rc = set_smem(kern, smem);
   if (rc) return rc;
@@ -104,6 +104,7 @@ int launch_variant(int v, const T *xp, LoopArgs la, int teams, int threads, Work
     case 14: if (bulk_ok) return launch_bulk<T, OP, 6, 16384>(xp, la, teams, threads, w, op, st); break;
     case 15: if (bulk_ok) return launch_bulk<T, OP, 2, 32768>(xp, la, teams, threads, w, op, st); break;
     case 16: if (bulk_ok) return launch_bulk<T, OP, 12, 8192>(xp, la, teams, threads, w, op, st); break;
+    case 17: if (bulk_ok) return launch_bulk<T, OP, 4, 32768, true>(xp, la, teams, threads, w, op, st); break;
     default: return fail(OMPRT_EINVAL, "unknown variant %d", v);
   }
   if (v >= 10) k_reduce<T, OP, 4><<<teams, threads, 0, st>>>(xp, la, w, op);

@@ -1,0 +1,33 @@
+"""Small launches of every kernel family for compute-sanitizer runs
+(memcheck / racecheck / synccheck / initcheck)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+from paper_2106_03219_b200 import _lib, runtime
+
+dev = torch.device("cuda", 0)
+S = 0x210603219
+x = runtime.synthetic(100_003, "f64", S, device=dev)
+xi = runtime.synthetic(100_003, "i64", S, device=dev)
+xf = runtime.synthetic(100_003, "f32", S, device=dev)
+yf = runtime.synthetic(100_003, "f32", S, 1, device=dev)
+for sched in ("static", "static_chunked", "distribute", "distribute_chunked"):
+    for mode in ("spmd", "ordered"):
+        runtime.reduce(x, sched=sched, chunk=64, teams=8, threads=256, mode=mode)
+        runtime.reduce(xi, "max", lb=3, ub=99_000, sched=sched, chunk=7, teams=5, threads=96, mode=mode)
+        runtime.axpy_minmax(0.5, xf, yf, sched=sched, chunk=64, teams=8, threads=256, mode=mode)
+        runtime.dot(x, x, sched=sched, chunk=64, teams=8, threads=256, mode=mode)
+runtime.set_unroll(8)
+runtime.reduce(x, teams=8, threads=256)
+runtime.set_unroll(4)
+runtime.bounds_dump(0, 99_999, "static_chunked", 3, teams=4, threads=64, device=dev)
+runtime.generic_reduce(xi, teams=16, par_threads=64)
+runtime.generic_reduce(xi, teams=16, par_threads=64, ordered=True)
+runtime.generic_reduce(xi, teams=4, par_threads=64, pad_bytes=65000, heap_fallback=True, heap_bytes_per_team=4096)
+runtime.check_trap(dev)
+runtime.arena_replay([[0, 100, 0], [0, 2000, 0], [1, 2000, 104], [1, 100, 0]], teams=2, threads=64, device=dev)
+runtime.atomic_probe(_lib.ATOMIC_ADD, "u32", list(range(64)), teams=2, threads=32, device=dev)
+runtime.atomic_apply(_lib.ATOMIC_CAS, "i64", [1, 2, 3], [1, 0, 3], [9, 9, 9], device=dev)
+torch.cuda.synchronize()
+print("sanitize driver done")
