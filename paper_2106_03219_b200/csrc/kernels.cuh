@@ -266,17 +266,49 @@ template <int OP, class T> OMPRT_D T fold_in_order(T acc, const T *p, int64_t n)
   return acc;
 }
 
+// The same fold with the whole (last) team staging the partials through
+// shared memory in coalesced chunks; thread 0 still adds them strictly in
+// order from shared memory (short-latency loads instead of one dependent
+// global load per partial).  Every thread of the team must call it; the
+// result is valid in thread 0.
+template <int OP, class T>
+OMPRT_D T fold_in_order_team(T acc, const T *p, int64_t n, T *buf, int cap) {
+  for (int64_t base = 0; base < n; base += cap) {
+    const int m = (int)((n - base) < cap ? (n - base) : cap);
+    for (int k = threadIdx.x; k < m; k += blockDim.x) buf[k] = ld_cg(p + base + k);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (; k + 8 <= m; k += 8) {
+        T v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = buf[k + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = Red<OP, T>::apply(acc, v[u]);
+      }
+      for (; k < m; ++k) acc = Red<OP, T>::apply(acc, buf[k]);
+    }
+    __syncthreads();
+  }
+  return acc;
+}
+
+constexpr int kFoldBuf = 2048;  // elements of the static fold buffer
+
 template <class T, int OP>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce_ordered(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
   T part = Red<OP, T>::identity();
   run_thread_chunks(la.sched, la.lb, la.ub, la.chunk,
                     [&](int64_t i) { part = Red<OP, T>::apply(part, x[i]); });
+  __shared__ T buf[kFoldBuf];
   T *tp = (T *)ws.thread_partials;
   tp[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = part;
   __syncthreads();
-  if (teams_ticket<OP, T>(part, (T *)ws.team_partials, ws.ticket) && threadIdx.x == 0) {
-    *out = fold_in_order<OP, T>(*out, tp, (int64_t)gridDim.x * blockDim.x);
+  if (teams_ticket<OP, T>(part, (T *)ws.team_partials, ws.ticket)) {
+    const T v = fold_in_order_team<OP, T>(threadIdx.x == 0 ? *out : part, tp,
+                                          (int64_t)gridDim.x * blockDim.x, buf, kFoldBuf);
+    if (threadIdx.x == 0) *out = v;
   }
 }
 
@@ -302,12 +334,14 @@ __global__ void __launch_bounds__(kMaxThreads)
   double part = 0.0;
   run_thread_chunks(la.sched, la.lb, la.ub, la.chunk,
                     [&](int64_t i) { part = __fma_rn(x[i], y[i], part); });
+  __shared__ double buf[kFoldBuf];
   double *tp = (double *)ws.thread_partials;
   tp[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = part;
   __syncthreads();
-  if (teams_ticket<OMPRT_OP_ADD, double>(part, (double *)ws.team_partials, ws.ticket) &&
-      threadIdx.x == 0) {
-    *out = fold_in_order<OMPRT_OP_ADD, double>(*out, tp, (int64_t)gridDim.x * blockDim.x);
+  if (teams_ticket<OMPRT_OP_ADD, double>(part, (double *)ws.team_partials, ws.ticket)) {
+    const double v = fold_in_order_team<OMPRT_OP_ADD, double>(
+        threadIdx.x == 0 ? *out : 0.0, tp, (int64_t)gridDim.x * blockDim.x, buf, kFoldBuf);
+    if (threadIdx.x == 0) *out = v;
   }
 }
 
@@ -352,10 +386,16 @@ __global__ void __launch_bounds__(kMaxThreads)
   tmax[g] = mx;
   tmin[g] = mn;
   __syncthreads();
-  if (teams_ticket<OMPRT_OP_MAX, float>(mx, (float *)ws.team_partials, ws.ticket) &&
-      threadIdx.x == 0) {
-    *out_max = fold_in_order<OMPRT_OP_MAX, float>(*out_max, tmax, n);
-    *out_min = fold_in_order<OMPRT_OP_MIN, float>(*out_min, tmin, n);
+  __shared__ float buf[kFoldBuf];
+  if (teams_ticket<OMPRT_OP_MAX, float>(mx, (float *)ws.team_partials, ws.ticket)) {
+    const float vmax = fold_in_order_team<OMPRT_OP_MAX, float>(
+        threadIdx.x == 0 ? *out_max : mx, tmax, n, buf, kFoldBuf);
+    const float vmin = fold_in_order_team<OMPRT_OP_MIN, float>(
+        threadIdx.x == 0 ? *out_min : mn, tmin, n, buf, kFoldBuf);
+    if (threadIdx.x == 0) {
+      *out_max = vmax;
+      *out_min = vmin;
+    }
   }
 }
 

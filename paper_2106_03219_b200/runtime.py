@@ -64,8 +64,16 @@ def _p(t: torch.Tensor | None) -> C.c_void_p:
     return C.c_void_p(0 if t is None else t.data_ptr())
 
 
+_sms: dict[int, int] = {}
+
+
 def num_sms() -> int:
-    return check(_lib.load().omprt_num_sms(), "omprt_num_sms")
+    """SM count of the current CUDA device (cached per device)."""
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+    n = _sms.get(dev)
+    if n is None:
+        n = _sms[dev] = check(_lib.load().omprt_num_sms(), "omprt_num_sms")
+    return n
 
 
 def set_unroll(unroll: int) -> None:

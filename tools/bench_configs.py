@@ -77,9 +77,11 @@ def main():
     outi = torch.zeros(1, dtype=torch.int64, device=dev)
     ms = timeit(lambda: runtime.reduce(xi, "max", out=outi), a.reps // 4)
     line("C2-int int64 max N=2^30", ms, n * 8)
-    ms = timeit(lambda: runtime.reduce(x, mode="ordered", teams=sms, threads=1024, out=outf), 5, 1)
-    line("C2 fp64 sum ORDERED (reference order, bit-exact) N=2^30", ms, n * 8,
-         teams=sms, threads=1024)
+    for thr in (1024, 256):
+        ms = timeit(lambda: runtime.reduce(x, mode="ordered", teams=sms, threads=thr, out=outf),
+                    10, 1)
+        line("C2 fp64 sum ORDERED (reference order, bit-exact) N=2^30", ms, n * 8,
+             teams=sms, threads=thr)
 
     # C5 shard: fp64 dot over 2^30 (16 B / iteration)
     y = runtime.synthetic(n, "f64", SEED, 1, device=dev)
