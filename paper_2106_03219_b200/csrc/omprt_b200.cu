@@ -11,7 +11,6 @@
 
 #include "bulk.cuh"
 #include "generic.cuh"
-#include "ordered.cuh"
 
 using namespace omprt;
 
@@ -122,24 +121,7 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
       return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
   }
   const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
-  const bool ordered_bulk = (la.sched == OMPRT_SCHED_STATIC || la.sched == OMPRT_SCHED_DISTRIBUTE) &&
-                            threads % 32 == 0 && threads >= 64 && threads <= 256 && g_unroll == 4;
-  if (mode == OMPRT_MODE_ORDERED && ordered_bulk) {
-    // literal per-thread order, rows streamed by bulk copies (ordered.cuh)
-    if (threads <= 128) {
-      auto kern = k_reduce_ordered_bulk<T, OP, 512>;
-      const size_t smem = OrderedGeom<512>::smem_bytes(threads);
-      int rc = set_smem(kern, smem);
-      if (rc) return rc;
-      kern<<<teams, threads, smem, st>>>(xp, la, w, op);
-    } else {
-      auto kern = k_reduce_ordered_bulk<T, OP, 256>;
-      const size_t smem = OrderedGeom<256>::smem_bytes(threads);
-      int rc = set_smem(kern, smem);
-      if (rc) return rc;
-      kern<<<teams, threads, smem, st>>>(xp, la, w, op);
-    }
-  } else if (mode == OMPRT_MODE_ORDERED) {
+  if (mode == OMPRT_MODE_ORDERED) {
     k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
   } else if (bulk_ok) {
     // default SPMD path for contiguous team sets: TMA bulk-copy stage ring
