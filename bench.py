@@ -66,7 +66,7 @@ def peaks() -> dict:
 def ncu_traffic():
     """dram read+write bytes per launch of the reduce kernel from the committed
     ncu --set full capture (profiles/), or None."""
-    f = ROOT / "profiles" / "ncu_reduce_f64.json"
+    f = ROOT / "profiles" / "ncu_bench_kernel.json"
     if f.exists():
         try:
             return json.loads(f.read_text()).get("dram_bytes_per_launch")

@@ -124,7 +124,7 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
   if (mode == OMPRT_MODE_ORDERED) {
     k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
   } else if (bulk_ok) {
-    // default SPMD path for contiguous team sets: TMA bulk-copy stage ring
+    // default SPMD path: TMA bulk-copy stage ring
     return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, threads, w, op, st);
   } else if (g_unroll >= 8) {
     k_reduce<T, OP, 8><<<teams, threads, 0, st>>>(xp, la, w, op);

@@ -215,3 +215,28 @@ def test_bulk_ring_stress(cuda):
             runtime.reduce(x, lb=lb, ub=ub, sched="distribute", teams=teams, threads=threads,
                            out=out)
         assert int(out.item()) == (want * 200 + 2**63) % 2**64 - 2**63
+
+
+@pytest.mark.parametrize("dtype", ["f64", "i32", "u64"])
+def test_comb_bulk_plans(cuda, dtype):
+    # flat schedule(static, c): teeth packed per stage (case B), cut into
+    # stages (case A), clipped last teeth, aligned and misaligned starts
+    dt = ALLDT[dtype]
+    n = 1_000_003
+    x = O.fill(n, dt, O.SEED, 5)
+    xd = torch.from_numpy(x).to(cuda)
+    V = 16 // x.itemsize
+    for teams, threads, chunk, lb, ub in ((7, 128, 3, 0, n - 3), (5, 64, 1, 0, n - 1),
+                                          (3, 256, 700, 0, n - 1), (9, 96, 64, V, n - 2),
+                                          (148, 256, 1, 0, n - 1), (2, 64, 4096, 0, 70_000),
+                                          (4, 128, 2, 1, n - 1)):
+        want = O.reduce(x, lb, ub, dt, O.ADD, O.STATIC_CHUNKED, chunk, teams, threads, 0)
+        out = torch.zeros(1, dtype=xd.dtype, device=cuda)
+        runtime.reduce(xd, lb=lb, ub=ub, sched="static_chunked", chunk=chunk, teams=teams,
+                       threads=threads, out=out)
+        got = out.cpu().numpy()[0]
+        if dt == O.F64:
+            exact = O.accurate_sum_f64(x[lb:ub + 1])
+            assert abs(float(got) - exact) <= 1e-9 * exact
+        else:
+            assert int(got) == int(want), (teams, threads, chunk, lb, ub)

@@ -3,5 +3,4 @@ set -x
 mkdir -p gpurun_out
 B="python bench.py --e2e-steps 0 --no-cpu-baseline"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv $B --steps 20 --warmup 2 > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reduce_bulk -s 3 -c 1 -o gpurun_out/prof_reduce_bulk $B --steps 5 --warmup 1 > gpurun_out/ncu_full.log 2>&1
-timeout 600 python bench.py --steps 1000 --warmup 10 > gpurun_out/bench.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reduce_bulk -s 3 -c 1 -o gpurun_out/prof_bench $B --steps 5 --warmup 1 > gpurun_out/ncu_full.log 2>&1

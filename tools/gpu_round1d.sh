@@ -1,4 +1,6 @@
 set -x
 mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider --maxfail=20 > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
 timeout 900 python tools/bench_configs.py > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
