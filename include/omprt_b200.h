@@ -258,6 +258,17 @@ int omprt_atomic_probe(int kind, int dtype, const uint64_t *d_operands,
                        const uint64_t *d_desired, uint64_t *d_cell, uint64_t *d_old,
                        int teams, int threads, void *stream);
 
+/* Per-thread atomic programs on one cell (corpus.probe_source, corpus.py:374-408):
+ * thread g of the (teams x threads) grid executes ops [d_offsets[g], d_offsets[g+1])
+ * in program order — kind d_kinds[k] (omprt_atomic_kind; every kind valid for
+ * dtype, INC only on U32), operand d_operands[k], desired d_desired[k] (CAS) —
+ * on *d_cell and writes the old value of op k to d_old[k].  d_offsets has
+ * teams*threads+1 entries; nops = d_offsets[teams*threads]. */
+int omprt_atomic_program(const int32_t *d_kinds, const uint64_t *d_operands,
+                         const uint64_t *d_desired, const int64_t *d_offsets, int64_t nops,
+                         int dtype, uint64_t *d_cell, uint64_t *d_old, int teams, int threads,
+                         void *stream);
+
 /* Batched step semantics: thread g applies one RMW of `kind` to its own cell
  * d_cells[g] (element type dtype, packed; i32/u32 cells are 4 bytes apart)
  * with operand d_operands[g] (d_desired[g] for CAS); the old value goes to

@@ -405,6 +405,47 @@ def run_probes():
     return probes
 
 
+def run_program_probes():
+    """Multi-op per-thread programs (corpus.probe_source) on vgpu, several seeds."""
+    rng = random.Random(0xA71)
+    out = []
+    kinds = ("add", "max", "xchg", "cas", "inc")
+    for mix in ("add", "max", "inc", "mixed", "mixed"):
+        for teams, threads in ((1, 4), (2, 4), (2, 3)):
+            progs = []
+            for _ in range(teams * threads):
+                ops = []
+                for _ in range(rng.randint(1, 3)):
+                    kind = rng.choice(kinds) if mix == "mixed" else mix
+                    e = 7 if kind == "inc" else rng.randint(0, 40)
+                    d = rng.randint(0, 40)
+                    if kind == "cas":
+                        e = rng.choice([0, 0, rng.randint(0, 40)])
+                    ops.append((kind, e, d))
+                progs.append(ops)
+            src = corpus.probe_source(teams, threads, progs)
+            mod = parse_module(src)
+            prog = HostProgram(mod)
+            img = compile_device_image(lower_atomics(copy.deepcopy(mod)), "vgpu")
+            call = prog.target_calls[0]
+            total = sum(len(p) for p in progs)
+            for seed in (0, 5, 11):
+                cell = le_bytes([0], "u32")
+                olds = le_bytes([0] * total, "u32")
+                st = tgt_target(call.bind(_bind(call, {"c": cell, "olds": olds})), {"vgpu": img},
+                                "vgpu", grid=(teams, threads), sched_seed=seed)
+                assert st == 0
+                flat = from_le(olds, "u32")
+                per, k = [], 0
+                for p in progs:
+                    per.append(flat[k:k + len(p)])
+                    k += len(p)
+                out.append({"mix": mix, "teams": teams, "threads": threads,
+                            "programs": [[list(op) for op in p] for p in progs],
+                            "sched_seed": seed, "cell": from_le(cell, "u32")[0], "olds": per})
+    return out
+
+
 def run_corpus():
     res = {}
     for name, src in corpus.CORPUS:
@@ -441,7 +482,8 @@ def fallback_runs(quick: bool) -> dict:
                run_generic(100, 8, 4, 0, 5), run_generic(2**13, 256, 4, 40, 7),
                run_generic(64, 2, 4, 65536 - 8, 6)]  # pad + parts overflows -> trap 1
     return {"seed": SEED, "reductions": reds, "vgpu_bounds": bounds, "generic": generic,
-            "probes": run_probes(), "corpus": run_corpus()}
+            "probes": run_probes(), "program_probes": run_program_probes(),
+            "corpus": run_corpus()}
 
 
 def main():

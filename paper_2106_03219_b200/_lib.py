@@ -83,6 +83,9 @@ _SIGS = {
                             C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "omprt_atomic_probe": ([C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "omprt_atomic_program": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                              C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p],
+                             C.c_int),
     "omprt_atomic_apply": ([C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_int64, C.c_void_p], C.c_int),
     "omprt_fill": ([C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_int, C.c_int64, C.c_void_p],

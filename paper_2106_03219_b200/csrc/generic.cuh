@@ -299,6 +299,22 @@ __global__ void k_atomic_probe(int kind, const uint64_t *__restrict__ ops,
   old_out[g] = as_word<T>(atomic_rmw<T>(kind, cell, (T)ops[g], d));
 }
 
+// Every thread runs its own program of RMWs on the single shared cell, in
+// program order (corpus.probe_source, corpus.py:374-408): thread g executes
+// ops [offsets[g], offsets[g+1]) and records each old value in its slot.
+template <class T>
+__global__ void k_atomic_program(const int32_t *__restrict__ kinds,
+                                 const uint64_t *__restrict__ ops,
+                                 const uint64_t *__restrict__ desired,
+                                 const int64_t *__restrict__ offsets, T *cell,
+                                 uint64_t *__restrict__ old_out) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t k = offsets[g]; k < offsets[g + 1]; ++k) {
+    const T d = desired ? (T)desired[k] : T(0);
+    old_out[k] = as_word<T>(atomic_rmw<T>(kinds[k], cell, (T)ops[k], d));
+  }
+}
+
 // Thread g applies one RMW to its own cell g (batched step_* semantics).
 template <class T>
 __global__ void k_atomic_apply(int kind, T *cells, const uint64_t *__restrict__ ops,

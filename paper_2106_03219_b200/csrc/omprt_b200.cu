@@ -228,6 +228,12 @@ template <class T> struct AtomicF {
     k_atomic_probe<T><<<teams, threads, 0, st>>>(kind, ops, desired, (T *)cell, old);
     return check_launch("omprt_atomic_probe");
   }
+  static int program(const int32_t *kinds, const uint64_t *ops, const uint64_t *desired,
+                     const int64_t *offsets, void *cell, uint64_t *old, int teams, int threads,
+                     cudaStream_t st) {
+    k_atomic_program<T><<<teams, threads, 0, st>>>(kinds, ops, desired, offsets, (T *)cell, old);
+    return check_launch("omprt_atomic_program");
+  }
   static int apply(int kind, void *cells, const uint64_t *ops, const uint64_t *desired,
                    uint64_t *old, int64_t n, cudaStream_t st) {
     if (n <= 0) return OMPRT_OK;
@@ -561,6 +567,34 @@ int omprt_atomic_apply(int kind, int dtype, uint64_t *d_cells, const uint64_t *d
       return AtomicF<int64_t>::apply(kind, d_cells, d_operands, d_desired, d_old, n, S(stream));
     default:
       return AtomicF<uint64_t>::apply(kind, d_cells, d_operands, d_desired, d_old, n, S(stream));
+  }
+}
+
+int omprt_atomic_program(const int32_t *d_kinds, const uint64_t *d_operands,
+                         const uint64_t *d_desired, const int64_t *d_offsets, int64_t nops,
+                         int dtype, uint64_t *d_cell, uint64_t *d_old, int teams, int threads,
+                         void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads))) return rc;
+  if (dtype != OMPRT_I32 && dtype != OMPRT_U32 && dtype != OMPRT_I64 && dtype != OMPRT_U64)
+    return fail(OMPRT_EINVAL, "atomics take i32/u32/i64/u64 (got dtype %d)", dtype);
+  if (!d_offsets || !d_cell || (nops > 0 && (!d_kinds || !d_operands || !d_old)))
+    return fail(OMPRT_EINVAL, "atomic_program: null pointer");
+  // kinds are validated on the host side of the ABI by the caller's table;
+  // INC on 64-bit cells and CAS without desired values are rejected here
+  switch (dtype) {
+    case OMPRT_I32:
+      return AtomicF<int32_t>::program(d_kinds, d_operands, d_desired, d_offsets, d_cell, d_old,
+                                       teams, threads, S(stream));
+    case OMPRT_U32:
+      return AtomicF<uint32_t>::program(d_kinds, d_operands, d_desired, d_offsets, d_cell, d_old,
+                                        teams, threads, S(stream));
+    case OMPRT_I64:
+      return AtomicF<int64_t>::program(d_kinds, d_operands, d_desired, d_offsets, d_cell, d_old,
+                                       teams, threads, S(stream));
+    default:
+      return AtomicF<uint64_t>::program(d_kinds, d_operands, d_desired, d_offsets, d_cell, d_old,
+                                        teams, threads, S(stream));
   }
 }
 

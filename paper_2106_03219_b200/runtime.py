@@ -330,6 +330,38 @@ def atomic_probe(kind: int, dtype, operands, desired=None, *, teams: int, thread
     return int(cell.cpu().item()), [int(v) for v in old.cpu().tolist()]
 
 
+def atomic_program(dtype, programs, *, teams: int, threads: int, init: int = 0,
+                   device="cuda") -> tuple[int, list[list[int]]]:
+    """programs[g] = [(kind, e, d), ...] for global thread g (corpus.probe_source
+    shape).  Returns (final cell, olds per thread in program order)."""
+    dt = dtype_code(dtype)
+    n = teams * threads
+    if len(programs) != n:
+        raise ValueError("one program per thread is required")
+    bits = 32 if dt in (_lib.I32, _lib.U32) else 64
+    if any(k == _lib.ATOMIC_INC for p in programs for k, _, _ in p) and dt != _lib.U32:
+        raise ValueError("atomic_inc is u32 only (runtime.mc:175-186)")
+    flat = [op for p in programs for op in p]
+    offs = [0]
+    for p in programs:
+        offs.append(offs[-1] + len(p))
+    kinds = torch.tensor([k for k, _, _ in flat] or [0], dtype=torch.int32, device=device)
+    dev = _dev(kinds)
+    ops = torch.tensor([e & (2**64 - 1) for _, e, _ in flat] or [0], dtype=torch.uint64,
+                       device=dev)
+    des = torch.tensor([d & (2**64 - 1) for _, _, d in flat] or [0], dtype=torch.uint64,
+                       device=dev)
+    off = torch.tensor(offs, dtype=torch.int64, device=dev)
+    cell = torch.tensor([init & (2**bits - 1)], dtype=torch.uint32 if bits == 32 else torch.uint64,
+                        device=dev)
+    old = torch.zeros(max(len(flat), 1), dtype=torch.uint64, device=dev)
+    check(_lib.load().omprt_atomic_program(_p(kinds), _p(ops), _p(des), _p(off), len(flat), dt,
+                                           _p(cell), _p(old), teams, threads, _stream(kinds)),
+          "omprt_atomic_program")
+    olds = [int(v) for v in old.cpu().tolist()]
+    return int(cell.cpu().item()), [olds[offs[g]:offs[g + 1]] for g in range(n)]
+
+
 def atomic_apply(kind: int, dtype, cells, operands, desired=None,
                  device="cuda") -> tuple[list[int], list[int]]:
     """Batched step semantics: returns (new cells, olds) as zero-extended words."""

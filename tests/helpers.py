@@ -53,6 +53,44 @@ def linearizable(kind: int, dtype: int, init: int, ops, desired, olds, final) ->
     return search(0, init)
 
 
+def linearizable_programs(dtype: int, init: int, programs, olds, final) -> bool:
+    """Per-thread programs of RMWs on one cell (programs[g] = [(kind, e, d)],
+    olds[g] = observed old values): is there an interleaving that respects
+    every thread's program order and reproduces all observations?  (SPEC
+    acceptance criterion 5; DFS over per-thread program counters.)"""
+    n = len(programs)
+    progs = [list(p) for p in programs]
+    obs = [list(o) for o in olds]
+
+    @lru_cache(maxsize=None)
+    def search(pcs: tuple, cell: int) -> bool:
+        pcs = list(pcs)
+        changed = True
+        while changed:  # ops that observe `cell` and keep it: place now (w.l.o.g.)
+            changed = False
+            for g in range(n):
+                k = pcs[g]
+                if k < len(progs[g]) and obs[g][k] == cell:
+                    kind, e, d = progs[g][k]
+                    if O.atomic_step(kind, dtype, cell, e, d)[0] == cell:
+                        pcs[g] += 1
+                        changed = True
+        if all(pcs[g] == len(progs[g]) for g in range(n)):
+            return cell == final
+        for g in range(n):
+            k = pcs[g]
+            if k < len(progs[g]) and obs[g][k] == cell:
+                kind, e, d = progs[g][k]
+                new, _ = O.atomic_step(kind, dtype, cell, e, d)
+                nxt = list(pcs)
+                nxt[g] += 1
+                if search(tuple(nxt), new):
+                    return True
+        return False
+
+    return search(tuple([0] * n), init)
+
+
 def fold_int(op: str, bits: int, signed: bool, init: int, vals) -> int:
     """Python restatement of the integer combine (wrap / signed compare)."""
     m = (1 << bits) - 1

@@ -15,7 +15,7 @@ import torch
 
 from oracle import oracle as O
 from paper_2106_03219_b200 import _lib, devicert, runtime
-from tests.helpers import KIND, linearizable
+from tests.helpers import KIND, linearizable, linearizable_programs
 
 pytestmark = pytest.mark.gpu
 
@@ -151,6 +151,34 @@ def test_atomic_probes_linearizable(cuda, fallback_golden):
         assert linearizable(kind, O.U32, 0, ops, des, olds, cell), p
         if p["kind"] in ("add", "max", "inc"):
             assert cell == p["cell"]
+
+
+def test_atomic_programs_linearizable(cuda, fallback_golden):
+    # the vgpu's per-thread multi-op programs on the device: every history
+    # respects program order; commutative programs end where vgpu ended
+    for p in fallback_golden["program_probes"]:
+        programs = [[(KIND[k], e, d) for k, e, d in prog] for prog in p["programs"]]
+        cell, olds = runtime.atomic_program("u32", programs, teams=p["teams"],
+                                            threads=p["threads"], device=cuda)
+        assert linearizable_programs(O.U32, 0, programs, olds, cell), p
+        if p["mix"] in ("add", "max", "inc"):
+            assert cell == p["cell"]
+
+
+def test_atomic_programs_typed(cuda):
+    # signed i64 programs: max/min compare signed, add wraps
+    rng = random.Random(9)
+    for dtype, dt in (("i64", O.I64), ("i32", O.I32), ("u64", O.U64)):
+        bits = 32 if dt == O.I32 else 64
+        progs = []
+        for _ in range(3 * 4):
+            ops = []
+            for _ in range(rng.randint(1, 3)):
+                kind = rng.choice([_lib.ATOMIC_ADD, _lib.ATOMIC_MAX, _lib.ATOMIC_MIN])
+                ops.append((kind, rng.getrandbits(bits), 0))
+            progs.append(ops)
+        cell, olds = runtime.atomic_program(dtype, progs, teams=3, threads=4, device=cuda)
+        assert linearizable_programs(dt, 0, progs, olds, cell)
 
 
 def test_inc_ring_modular(cuda):

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.helpers import DT, KIND, OPS, linearizable
+from tests.helpers import DT, KIND, OPS, linearizable, linearizable_programs
 
 
 def test_static_bounds_matches_reference(devicert_golden):
@@ -129,6 +129,19 @@ def test_vgpu_probe_histories_are_linearizable(fallback_golden):
         ops = [o[0] for o in p["ops"]]
         des = [o[1] for o in p["ops"]]
         assert linearizable(KIND[p["kind"]], O.U32, 0, ops, des, p["olds"], p["cell"]), p
+
+
+def test_vgpu_program_histories_are_linearizable(fallback_golden):
+    # multi-op programs per thread (corpus.probe_source): program order holds
+    progs = fallback_golden["program_probes"]
+    assert len(progs) >= 40
+    for p in progs:
+        programs = [[(KIND[k], e, d) for k, e, d in prog] for prog in p["programs"]]
+        assert linearizable_programs(O.U32, 0, programs, p["olds"], p["cell"]), p
+        # and a corrupted history is rejected
+        bad = [list(o) for o in p["olds"]]
+        bad[0][0] ^= 0x100
+        assert not linearizable_programs(O.U32, 0, programs, bad, p["cell"])
 
 
 def test_corpus_outputs_agree(fallback_golden):
