@@ -101,7 +101,12 @@ enum omprt_atomic_kind {
 };
 
 /* ---- arena script opcodes for omprt_arena_replay */
-enum omprt_arena_op { OMPRT_ARENA_ALLOC = 0, OMPRT_ARENA_FREE = 1 };
+enum omprt_arena_op {
+  OMPRT_ARENA_ALLOC = 0,
+  OMPRT_ARENA_FREE = 1,
+  OMPRT_ARENA_WRITE = 2,
+  OMPRT_ARENA_READ = 3
+};
 
 #define OMPRT_ARENA_CAPACITY 65536 /* devicert.ARENA_CAPACITY, devicert.py:54 */
 #define OMPRT_ARENA_ALIGN 8        /* devicert.ARENA_ALIGN,    devicert.py:55 */
@@ -234,20 +239,26 @@ int omprt_generic_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int
 /* Shared-memory smart stack and atomics (parity probes)                      */
 /* ========================================================================= */
 
-/* Replays an alloc/free script on the device arena of every team.
- * d_script: nops x 3 int64 {opcode (omprt_arena_op), bytes, offset(for free)}.
- * Each team executes the script from thread `caller_tid` (3 = NonUniformAlloc
- * when it is not 0) against its shared-memory arena (capacity bytes, <= 64 KiB
- * plus heap spill if heap_fallback).  d_results: teams x nops int64 — the
- * offset for an alloc, 0 for a free, -code at the trapping op (later ops -0x7fff).
- * After each alloc every thread of the team writes and re-reads a tag pattern
- * through the returned offset (data-path check; mismatch -> trap Abort).
+/* Replays an arena script on the device arena of every team.
+ * d_script: nops x 4 int64 {opcode (omprt_arena_op), bytes, offset, value}:
+ *   ALLOC bytes -> offset; FREE bytes, offset -> 0; WRITE bytes, offset, value
+ *   (the team stores the little-endian u64 `value`, repeated) -> 0;
+ *   READ 8, offset -> the u64 there.
+ * Each team executes the script (ALLOC/FREE/READ from thread `caller_tid`;
+ * 3 = NonUniformAlloc when it is not 0) against its shared-memory arena
+ * (capacity bytes, <= 64 KiB, plus heap spill if heap_fallback), initialised
+ * to the 0xAA loader_uninitialized poison.  d_results: teams x nops int64 —
+ * the op's result, -code at the trapping op (later ops -0x7fff).  After each
+ * alloc every thread writes and re-reads a tag through the returned offset
+ * and restores the bytes (data-path check; mismatch -> trap Abort).
+ * check_uninit != 0: a READ of any byte no WRITE covered traps
+ * UninitializedRead (kind 4; vgpu's check_uninit, vgpu.py:365-369).
  * Synchronises; returns OMPRT_TRAP if any team trapped (the trap word is
  * left set for omprt_check_trap), else OMPRT_OK. */
 int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads,
                        int caller_tid, int64_t capacity, int heap_fallback,
-                       int64_t heap_bytes_per_team, void *d_heap, int64_t *d_results,
-                       void *stream);
+                       int64_t heap_bytes_per_team, void *d_heap, int check_uninit,
+                       int64_t *d_results, void *stream);
 
 /* Every thread of a (teams x threads) grid applies one atomic RMW of `kind`
  * (omprt_atomic_kind) to the single cell *d_cell (dtype I32/U32/I64/U64),

@@ -405,6 +405,57 @@ def run_probes():
     return probes
 
 
+UNINIT_SRC = """\
+#pragma omp begin declare target
+extern u64 __shared_arena[8192];
+#pragma omp end declare target
+
+void kernel(u64 *out, i64 w, i64 r, u64 v, i64 pad) {
+  #pragma omp target
+  {
+    u64 off;
+    u64 poff;
+    if (omp_thread_id() == 0) {
+      if (pad > 0) {
+        poff = __kmpc_alloc_shared((u64) pad);
+      }
+      off = __kmpc_alloc_shared(64);
+      __shared_arena[off / 8 + (u64) w] = v;
+      out[0] = __shared_arena[off / 8 + (u64) r];
+      out[1] = off;
+      __kmpc_free_shared(off, 64);
+      if (pad > 0) {
+        __kmpc_free_shared(poff, (u64) pad);
+      }
+    }
+  }
+}
+"""
+
+
+def run_uninit():
+    """The arena's data on vgpu: loader_uninitialized poison and check_uninit
+    (vgpu.py:64-77, 365-369)."""
+    prog, call, img = _prog(UNINIT_SRC)
+    out = []
+    for w, r, pad in ((0, 0, 0), (1, 3, 0), (2, 2, 24), (7, 6, 8), (5, 5, 0)):
+        for check in (True, False):
+            buf = le_bytes([0, 0], "u64")
+            sink = {}
+            st = tgt_target(call.bind(_bind(call, {"out": buf, "w": w, "r": r,
+                                                   "v": 0x1234567890ABCDEF, "pad": pad})),
+                            {"vgpu": img}, "vgpu", grid=(2, 4), sched_seed=1, check_uninit=check,
+                            out=sink)
+            rec = {"w": w, "r": r, "pad": pad, "value": 0x1234567890ABCDEF, "check": check,
+                   "status": st}
+            if st == 0:
+                rec["read"], rec["off"] = from_le(buf, "u64")
+            else:
+                rec["trap"] = sink["trap"][0]
+            out.append(rec)
+    return out
+
+
 def run_program_probes():
     """Multi-op per-thread programs (corpus.probe_source) on vgpu, several seeds."""
     rng = random.Random(0xA71)
@@ -483,6 +534,7 @@ def fallback_runs(quick: bool) -> dict:
                run_generic(64, 2, 4, 65536 - 8, 6)]  # pad + parts overflows -> trap 1
     return {"seed": SEED, "reductions": reds, "vgpu_bounds": bounds, "generic": generic,
             "probes": run_probes(), "program_probes": run_program_probes(),
+            "uninit": run_uninit(),
             "corpus": run_corpus()}
 
 

@@ -483,22 +483,54 @@ int oracle_generic_reduce(const void *x, uint64_t seed, int k, int64_t lb, int64
 
 /* devicert.Arena (devicert.py:124-148) + the runtime's thread-0 check
  * (runtime.mc:76, 87 -> trap 3) + the heap-fallback extension (one LIFO
- * stack continuing past `capacity` into a heap of heap_cap bytes).
- * script: nops x {op (0 alloc, 1 free), bytes, offset}.  results: offset,
- * 0 for free, -code at the trapping op, -0x7fff after it.  Returns the trap
- * code (0 if none). */
+ * stack continuing past `capacity` into a heap of heap_cap bytes) + the
+ * arena's data: 0xAA loader_uninitialized poison (vgpu.py:64-77), WRITE /
+ * READ ops, and vgpu's check_uninit shadow (vgpu.py:365-369, trap 4) over the
+ * shared-memory part.  script: nops x {op (0 alloc, 1 free, 2 write, 3 read),
+ * bytes, offset, value}.  results: offset / 0 / 0 / u64 read, -code at the
+ * trapping op, -0x7fff after it.  Returns the trap code (0 if none). */
 int oracle_arena_replay(const int64_t *script, int nops, int caller_tid, int64_t capacity,
-                        int heap_fallback, int64_t heap_cap, int64_t *results) {
+                        int heap_fallback, int64_t heap_cap, int check_uninit,
+                        int64_t *results) {
   uint64_t cursor = 0, heap_cursor = 0;
   int code = 0;
+  int64_t total = capacity + (heap_fallback ? heap_cap : 0);
+  unsigned char *mem = (unsigned char *)malloc((size_t)(total > 0 ? total : 1));
+  unsigned char *shadow = (unsigned char *)calloc((size_t)(capacity > 0 ? capacity : 1), 1);
+  memset(mem, 0xAA, (size_t)(total > 0 ? total : 1));
   for (int op = 0; op < nops; ++op) {
     if (code) {
       results[op] = -0x7fff;
       continue;
     }
-    int64_t kind = script[3 * op];
-    uint64_t bytes = (uint64_t)script[3 * op + 1], off = (uint64_t)script[3 * op + 2];
+    const int64_t *o = script + 4 * op;
+    int64_t kind = o[0];
+    uint64_t bytes = (uint64_t)o[1], off = (uint64_t)o[2], value = (uint64_t)o[3];
     uint64_t need = (bytes + 7) / 8 * 8;
+    if (kind == 2) { /* WRITE: little-endian value repeated by address */
+      for (uint64_t j = 0; j < bytes; ++j) {
+        uint64_t b = off + j;
+        mem[b] = (unsigned char)((value >> (8 * (b & 7))) & 0xff);
+        if ((int64_t)b < capacity) shadow[b] = 1;
+      }
+      results[op] = 0;
+      continue;
+    }
+    if (kind == 3) { /* READ of (up to) 8 bytes */
+      uint64_t v = 0;
+      int init = 1;
+      for (uint64_t j = 0; j < 8 && j < bytes; ++j) {
+        v |= (uint64_t)mem[off + j] << (8 * j);
+        if ((int64_t)(off + j) < capacity && !shadow[off + j]) init = 0;
+      }
+      if (check_uninit && !init) {
+        code = 4;
+        results[op] = -4;
+      } else {
+        results[op] = (int64_t)v;
+      }
+      continue;
+    }
     if (caller_tid != 0) {
       code = 3;
     } else if (kind == 0) {
@@ -533,6 +565,8 @@ int oracle_arena_replay(const int64_t *script, int nops, int caller_tid, int64_t
     }
     results[op] = -code;
   }
+  free(mem);
+  free(shadow);
   return code;
 }
 

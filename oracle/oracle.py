@@ -74,7 +74,7 @@ def lib():
         L.oracle_accurate_dot_gen.restype = C.c_double
         L.oracle_generic_reduce.argtypes = [vp, u64, C.c_int, i64, i64, C.c_int, C.c_int, i64,
                                             i64, vp]
-        L.oracle_arena_replay.argtypes = [vp, C.c_int, C.c_int, i64, C.c_int, i64, vp]
+        L.oracle_arena_replay.argtypes = [vp, C.c_int, C.c_int, i64, C.c_int, i64, C.c_int, vp]
         L.oracle_atomic_step.argtypes = [C.c_int, C.c_int, u64, u64, u64, C.POINTER(u64),
                                          C.POINTER(u64)]
         L.oracle_set_threads.argtypes = [C.c_int]
@@ -191,12 +191,14 @@ def generic_reduce(x, lb: int, ub: int, dtype: int, op: int, teams: int, P: int,
 # ---- arena / atomics
 
 def arena_replay(script, caller_tid: int = 0, capacity: int = 65536, heap_fallback: bool = False,
-                 heap_cap: int = 0) -> tuple[list[int], int]:
-    s = np.ascontiguousarray(np.asarray(script, dtype=np.int64).reshape(-1, 3))
-    res = np.zeros(len(s), dtype=np.int64)
+                 heap_cap: int = 0, check_uninit: bool = False) -> tuple[list[int], int]:
+    """script rows: (op, bytes, offset[, value]); ops 0 alloc 1 free 2 write 3 read."""
+    rows = [list(r) + [0] * (4 - len(r)) for r in script]
+    s = np.ascontiguousarray(np.asarray(rows, dtype=np.int64).reshape(-1, 4))
+    res = np.zeros(max(len(s), 1), dtype=np.int64)
     code = lib().oracle_arena_replay(_ptr(s), len(s), caller_tid, capacity, int(heap_fallback),
-                                     heap_cap, _ptr(res))
-    return [int(v) for v in res], int(code)
+                                     heap_cap, int(check_uninit), _ptr(res))
+    return [int(v) for v in res[:len(s)]], int(code)
 
 
 def atomic_step(kind: int, dtype: int, x: int, e: int, d: int = 0) -> tuple[int, int]:

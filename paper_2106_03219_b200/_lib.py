@@ -21,7 +21,7 @@ OP_ADD, OP_MAX, OP_MIN = range(3)
 SCHED_STATIC, SCHED_STATIC_CHUNKED, SCHED_DISTRIBUTE, SCHED_DISTRIBUTE_CHUNKED = range(4)
 MODE_SPMD, MODE_ORDERED = range(2)
 ATOMIC_ADD, ATOMIC_MAX, ATOMIC_MIN, ATOMIC_XCHG, ATOMIC_CAS, ATOMIC_INC = range(6)
-ARENA_ALLOC, ARENA_FREE = range(2)
+ARENA_ALLOC, ARENA_FREE, ARENA_WRITE, ARENA_READ = range(4)
 OK, FALLBACK, TRAP = 0, 1, 2
 EINVAL, ECUDA, ENOMEM = -1, -2, -3
 ARENA_CAPACITY = 65536
@@ -80,7 +80,7 @@ _SIGS = {
                               C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int64, C.c_void_p,
                               C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "omprt_arena_replay": ([C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
-                            C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+                            C.c_int64, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "omprt_atomic_probe": ([C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_int, C.c_int, C.c_void_p], C.c_int),
     "omprt_atomic_program": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,

@@ -91,51 +91,109 @@ OMPRT_D void arena_init(ArenaState &a, const ArenaCfg &c, unsigned char *smem) {
   a.heap_fallback = c.heap_fallback;
 }
 
-// Replay an alloc/free script (devicert.Arena parity; test_devicert.py:114-208).
-// Results per op: offset (alloc), 0 (free), -code at the trapping op and
-// kArenaSkipped after it.
+// Replay an arena script (devicert.Arena parity; test_devicert.py:114-208).
+// Script ops, 4 x int64 {opcode, bytes, offset, value}:
+//   ALLOC bytes                 -> the offset
+//   FREE  bytes, offset         -> 0
+//   WRITE bytes, offset, value  -> 0; the team stores `value` (little-endian
+//                                  u64, repeated) over [offset, offset+bytes)
+//   READ  bytes(=8), offset     -> the u64 at offset (int64 bits)
+// -code at the trapping op, kArenaSkipped after it.  The arena starts as
+// loader_uninitialized poison (0xAA, vgpu.py:64-77).  With check_uninit a
+// shadow bit per arena byte tracks WRITEs, and a READ touching an unwritten
+// byte traps UninitializedRead (kind 4, vgpu.py:365-369).  Heap-spilled
+// offsets (heap_fallback) are not shadowed.
 constexpr int64_t kArenaSkipped = -0x7fff;
 
 __global__ void k_arena_replay(const int64_t *__restrict__ script, int nops, int caller_tid,
-                               ArenaCfg cfg, int64_t *__restrict__ results) {
+                               ArenaCfg cfg, int check_uninit, int64_t *__restrict__ results) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ ArenaState st;
   __shared__ int64_t s_res;
-  // loader_uninitialized poison (vgpu.py:64-77 POISON_BYTE 0xAA)
+  __shared__ int s_trapped;
+  __shared__ uint32_t shadow[OMPRT_ARENA_CAPACITY / 32];
   for (int64_t i = threadIdx.x; i < cfg.capacity; i += blockDim.x) dsm[i] = 0xAA;
-  if (threadIdx.x == 0) arena_init(st, cfg, dsm);
+  for (int i = threadIdx.x; i < OMPRT_ARENA_CAPACITY / 32; i += blockDim.x) shadow[i] = 0;
+  if (threadIdx.x == 0) {
+    arena_init(st, cfg, dsm);
+    s_trapped = 0;
+  }
   __syncthreads();
   int64_t *res = results + (int64_t)blockIdx.x * nops;
   for (int op = 0; op < nops; ++op) {
-    const int64_t kind = script[3 * op], bytes = script[3 * op + 1], foff = script[3 * op + 2];
-    if (threadIdx.x == (uint32_t)caller_tid) {
+    const int64_t *o = script + 4 * op;
+    const int64_t kind = o[0], bytes = o[1], foff = o[2], value = o[3];
+    if (kind == OMPRT_ARENA_WRITE) {
+      // every thread of the team stores part of the range
+      unsigned char *p = arena_ptr(st, (uint64_t)foff);
+      for (int64_t j = threadIdx.x; j < bytes; j += blockDim.x) {
+        p[j] = (unsigned char)(((uint64_t)value >> (8 * ((foff + j) & 7))) & 0xffu);
+        const int64_t b = foff + j;
+        if (b < (int64_t)st.capacity) atomicOr(&shadow[b >> 5], 1u << (b & 31));
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) res[op] = 0;
+      continue;
+    }
+    if (kind == OMPRT_ARENA_READ) {
+      if (threadIdx.x == (uint32_t)caller_tid) {
+        const unsigned char *p = arena_ptr(st, (uint64_t)foff);
+        uint64_t v = 0;
+        bool init = true;
+        for (int j = 0; j < 8 && j < bytes; ++j) {
+          v |= (uint64_t)p[j] << (8 * j);
+          const int64_t b = foff + j;
+          if (b < (int64_t)st.capacity && !((shadow[b >> 5] >> (b & 31)) & 1u)) init = false;
+        }
+        s_res = (int64_t)v;
+        if (check_uninit && !init) {
+          s_res = -OMPRT_TRAP_UNINITIALIZED_READ;
+          s_trapped = 1;
+          raise_trap(OMPRT_TRAP_UNINITIALIZED_READ, 0);
+        }
+      }
+    } else if (threadIdx.x == (uint32_t)caller_tid) {
       // the calling thread runs the runtime routine with its own thread id
       s_res = (kind == OMPRT_ARENA_ALLOC)
                   ? kmpc_alloc_shared(st, (uint64_t)bytes, threadIdx.x)
                   : kmpc_free_shared(st, (uint64_t)foff, (uint64_t)bytes, threadIdx.x);
-      if (s_res < 0) raise_trap((int)-s_res, (int)-s_res);
+      if (s_res < 0) {
+        s_trapped = 1;
+        raise_trap((int)-s_res, (int)-s_res);
+      }
     }
     __syncthreads();
     const int64_t r = s_res;
+    const int trapped = s_trapped;
     __syncthreads();  // every thread has read s_res before the next op rewrites it
     if (threadIdx.x == 0) res[op] = r;
-    if (r < 0) {
+    if (trapped) {
       if (threadIdx.x == 0)
         for (int k = op + 1; k < nops; ++k) res[k] = kArenaSkipped;
       return;
     }
     if (kind == OMPRT_ARENA_ALLOC && bytes > 0) {
-      // data path: the whole team writes a tag through the returned offset,
-      // then reads it back with a different thread->byte mapping
+      // data path: the team writes a tag through the returned offset and
+      // reads it back with another thread->byte mapping, one blockDim-sized
+      // window at a time, restoring the window's previous bytes afterwards
+      // (an allocation does not initialise memory)
       unsigned char *p = arena_ptr(st, (uint64_t)r);
       const unsigned tag = (unsigned)(blockIdx.x * 131u + op * 17u);
-      for (int64_t j = threadIdx.x; j < bytes; j += blockDim.x)
-        p[j] = (unsigned char)((tag + (unsigned)j) & 0xffu);
-      __syncthreads();
-      for (int64_t j = (int64_t)blockDim.x - 1 - threadIdx.x; j < bytes; j += blockDim.x)
-        if (j >= 0 && p[j] != (unsigned char)((tag + (unsigned)j) & 0xffu))
+      for (int64_t w = 0; w < bytes; w += blockDim.x) {
+        const int64_t j = w + threadIdx.x;
+        unsigned char orig = 0;
+        if (j < bytes) {
+          orig = p[j];
+          p[j] = (unsigned char)((tag + (unsigned)j) & 0xffu);
+        }
+        __syncthreads();
+        const int64_t k = w + (int64_t)blockDim.x - 1 - threadIdx.x;
+        if (k < bytes && p[k] != (unsigned char)((tag + (unsigned)k) & 0xffu))
           raise_trap(OMPRT_TRAP_ABORT, 0);
-      __syncthreads();
+        __syncthreads();
+        if (j < bytes) p[j] = orig;
+        __syncthreads();
+      }
     }
   }
 }

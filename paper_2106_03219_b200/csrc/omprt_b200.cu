@@ -498,8 +498,8 @@ int omprt_generic_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int
 
 int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads,
                        int caller_tid, int64_t capacity, int heap_fallback,
-                       int64_t heap_bytes_per_team, void *d_heap, int64_t *d_results,
-                       void *stream) {
+                       int64_t heap_bytes_per_team, void *d_heap, int check_uninit,
+                       int64_t *d_results, void *stream) {
   int rc;
   if ((rc = check_grid(teams, threads))) return rc;
   if (nops < 0 || (nops > 0 && (!d_script || !d_results)))
@@ -521,7 +521,8 @@ int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads
   if (smem > 48 * 1024)
     OMPRT_CUDA(cudaFuncSetAttribute(k_arena_replay, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
-  k_arena_replay<<<teams, threads, smem, S(stream)>>>(d_script, nops, caller_tid, cfg, d_results);
+  k_arena_replay<<<teams, threads, smem, S(stream)>>>(d_script, nops, caller_tid, cfg,
+                                                      check_uninit ? 1 : 0, d_results);
   if ((rc = check_launch("omprt_arena_replay"))) return rc;
   // report (but leave) the trap word: omprt_check_trap reads and clears it
   OMPRT_CUDA(cudaStreamSynchronize(S(stream)));

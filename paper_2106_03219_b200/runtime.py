@@ -292,10 +292,14 @@ def generic_reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = N
 
 def arena_replay(script, *, teams: int = 1, threads: int = 32, caller_tid: int = 0,
                  capacity: int = _lib.ARENA_CAPACITY, heap_fallback: bool = False,
-                 heap_bytes_per_team: int = 0, device="cuda") -> tuple[torch.Tensor, DeviceTrap | None]:
-    """Run an alloc/free script ([(op, bytes, offset), ...]) on every team's
-    device arena.  Returns (results [teams, nops] int64, trap or None)."""
-    s = torch.as_tensor(script, dtype=torch.int64).reshape(-1, 3).to(device)
+                 heap_bytes_per_team: int = 0, check_uninit: bool = False,
+                 device="cuda") -> tuple[torch.Tensor, DeviceTrap | None]:
+    """Run an arena script ([(op, bytes, offset[, value]), ...], see
+    omprt_arena_replay) on every team's device arena.  Returns
+    (results [teams, nops] int64, trap or None)."""
+    rows = [list(r) + [0] * (4 - len(r)) for r in script]
+    s = torch.tensor(rows or [[0, 0, 0, 0]], dtype=torch.int64).reshape(-1, 4)[: len(rows)]
+    s = s.to(device)
     dev = _dev(s)
     nops = s.shape[0]
     res = torch.zeros((teams, max(nops, 1)), dtype=torch.int64, device=dev)
@@ -304,7 +308,7 @@ def arena_replay(script, *, teams: int = 1, threads: int = 32, caller_tid: int =
         heap = torch.zeros(max(teams * heap_bytes_per_team, 16), dtype=torch.uint8, device=dev)
     st = _lib.load().omprt_arena_replay(_p(s), nops, teams, threads, caller_tid, capacity,
                                         int(heap_fallback), heap_bytes_per_team, _p(heap),
-                                        _p(res), _stream(s))
+                                        int(check_uninit), _p(res), _stream(s))
     check(st, "omprt_arena_replay")
     trap = check_trap(dev) if st == _lib.TRAP else None
     return res[:, :nops], trap

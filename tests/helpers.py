@@ -109,3 +109,18 @@ def fold_int(op: str, bits: int, signed: bool, init: int, vals) -> int:
         else:
             acc = v if acc > v else acc
     return acc
+
+
+def uninit_script(rec) -> tuple[list, int]:
+    """The vgpu check_uninit golden (gen_golden.UNINIT_SRC) as an arena script;
+    returns (script, index of the READ op)."""
+    script = []
+    if rec["pad"]:
+        script.append([0, rec["pad"], 0, 0])
+    off = (rec["pad"] + 7) // 8 * 8
+    v = rec["value"] - (1 << 64) if rec["value"] >> 63 else rec["value"]
+    script += [[0, 64, 0, 0], [2, 8, off + 8 * rec["w"], v], [3, 8, off + 8 * rec["r"], 0],
+               [1, 64, off, 0]]
+    if rec["pad"]:
+        script.append([1, rec["pad"], 0, 0])
+    return script, 3 if rec["pad"] else 2

@@ -15,7 +15,7 @@ import torch
 
 from oracle import oracle as O
 from paper_2106_03219_b200 import _lib, devicert, runtime
-from tests.helpers import KIND, linearizable, linearizable_programs
+from tests.helpers import KIND, linearizable, linearizable_programs, uninit_script
 
 pytestmark = pytest.mark.gpu
 
@@ -32,6 +32,20 @@ def test_arena_traces_match_reference(cuda, devicert_golden):
             assert trap is not None and trap.kind == t["code"] and trap.code == t["code"]
         else:
             assert trap is None
+
+
+def test_arena_check_uninit_matches_vgpu(cuda, fallback_golden):
+    for r in fallback_golden["uninit"]:
+        script, k = uninit_script(r)
+        res, trap = runtime.arena_replay(script, teams=2, threads=64, check_uninit=r["check"],
+                                         device=cuda)
+        if r["status"] == 2:
+            assert trap is not None and trap.kind == 4
+            assert res[0, k].item() == -4 and res[0, k + 1].item() == -0x7FFF
+        else:
+            assert trap is None
+            assert res[0, k].item() % (1 << 64) == r["read"]
+            assert res[1, k].item() % (1 << 64) == r["read"]
 
 
 def test_arena_non_uniform_alloc_traps(cuda):

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.helpers import DT, KIND, OPS, linearizable, linearizable_programs
+from tests.helpers import DT, KIND, OPS, linearizable, linearizable_programs, uninit_script
 
 
 def test_static_bounds_matches_reference(devicert_golden):
@@ -84,6 +84,20 @@ def test_arena_heap_fallback_extension():
     res, code = O.arena_replay([[0, 65528, 0], [0, 64, 0], [1, 65528, 0]], heap_fallback=True,
                                heap_cap=1 << 20)
     assert code == 2
+
+
+def test_arena_data_and_check_uninit_match_vgpu(fallback_golden):
+    # poison 0xAA, writes, and vgpu's check_uninit trap (vgpu.py:64-77, 365-369)
+    recs = fallback_golden["uninit"]
+    assert any(r["status"] == 2 for r in recs) and any(r["status"] == 0 for r in recs)
+    for r in recs:
+        script, k = uninit_script(r)
+        res, code = O.arena_replay(script, check_uninit=r["check"])
+        if r["status"] == 2:
+            assert r["trap"] == "UninitializedRead" and code == 4 and res[k] == -4
+        else:
+            assert code == 0 and res[k] % (1 << 64) == r["read"], r
+            assert res[k - 2] == r["off"]  # the alloc returned vgpu's offset
 
 
 def test_generator_c_matches_python():
