@@ -310,6 +310,31 @@ int omprt_reduce_host(const void *h_x, int64_t n, int dtype, int op, int sched,
 /* Release the buffers cached by omprt_reduce_host. */
 int omprt_release_host_cache(void);
 
+/* ========================================================================= */
+/* Compiled target regions (B200 device images)                               */
+/* ========================================================================= */
+
+/* Load an sm_100a cubin produced by the region compiler
+ * (paper_2106_03219_b200/regionc.py: forge IR image -> CUDA C++ over
+ * csrc/region_rt.cuh -> NVRTC) into the current context.  Replaces parsing a
+ * device image for the runnable arch (host._image_for, host.py:233-252, and
+ * VirtualGPU construction, vgpu.py:154-167).  *handle is opaque. */
+int omprt_image_load(const void *image, size_t bytes, void **handle);
+
+/* Unload an image loaded by omprt_image_load. */
+int omprt_image_unload(void *handle);
+
+/* Launch kernel `kernel` (an __omp_offload_<id> entry) of a loaded image on a
+ * (teams x threads) grid with `shared_bytes` of dynamic shared memory (the
+ * image's team-shared globals).  `argv` is the kernel's single by-value
+ * parameter block of argv_bytes (u64 words: trap record, global-space blob,
+ * its init shadow, the team-shared init shadow, the dead-barrier wait mask,
+ * then per IR parameter: buffer -> device pointer, byte length, vgpu offset;
+ * scalar -> masked value).  Replaces VirtualGPU.launch (vgpu.py:254-347).
+ * Stream-ordered, asynchronous: the trap record is read by the caller. */
+int omprt_image_launch(void *handle, const char *kernel, int teams, int threads,
+                       size_t shared_bytes, const void *argv, size_t argv_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,10 @@ _SIGS = {
     "omprt_reduce_host": ([C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
                            C.c_int, C.c_int, C.c_void_p], C.c_int),
     "omprt_release_host_cache": ([], C.c_int),
+    "omprt_image_load": ([C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)], C.c_int),
+    "omprt_image_unload": ([C.c_void_p], C.c_int),
+    "omprt_image_launch": ([C.c_void_p, C.c_char_p, C.c_int, C.c_int, C.c_size_t, C.c_void_p,
+                            C.c_size_t, C.c_void_p], C.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -659,4 +659,44 @@ int omprt_release_host_cache(void) {
   return OMPRT_OK;
 }
 
+// ------------------------------------------------------- compiled regions
+
+int omprt_image_load(const void *image, size_t bytes, void **handle) {
+  if (!image || !bytes || !handle) return fail(OMPRT_EINVAL, "image_load: bad arguments");
+  cudaLibrary_t lib = nullptr;
+  OMPRT_CUDA(cudaLibraryLoadData(&lib, image, nullptr, nullptr, 0, nullptr, nullptr, 0));
+  *handle = reinterpret_cast<void *>(lib);
+  return OMPRT_OK;
+}
+
+int omprt_image_unload(void *handle) {
+  if (!handle) return fail(OMPRT_EINVAL, "image_unload: null handle");
+  OMPRT_CUDA(cudaLibraryUnload(reinterpret_cast<cudaLibrary_t>(handle)));
+  return OMPRT_OK;
+}
+
+int omprt_image_launch(void *handle, const char *kernel, int teams, int threads,
+                       size_t shared_bytes, const void *argv, size_t argv_bytes, void *stream) {
+  if (!handle || !kernel || !argv || !argv_bytes)
+    return fail(OMPRT_EINVAL, "image_launch: bad arguments");
+  // GridConfig limits (vgpu.py:50-61)
+  if (teams < 1 || teams > 1024 || threads < 1 || threads > 1024)
+    return fail(OMPRT_EINVAL, "image_launch: grid %dx%d outside 1..1024", teams, threads);
+  cudaKernel_t k = nullptr;
+  cudaError_t e = cudaLibraryGetKernel(&k, reinterpret_cast<cudaLibrary_t>(handle), kernel);
+  if (e != cudaSuccess)
+    return fail(OMPRT_EINVAL, "image_launch: no kernel '%s' in the image (%s)", kernel,
+                cudaGetErrorString(e));
+  if (shared_bytes > 48 * 1024) {
+    int dev = 0;
+    OMPRT_CUDA(cudaGetDevice(&dev));
+    OMPRT_CUDA(cudaKernelSetAttributeForDevice(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)shared_bytes, dev));
+  }
+  void *params[1] = {const_cast<void *>(argv)};
+  OMPRT_CUDA(cudaLaunchKernel(reinterpret_cast<const void *>(k), dim3(teams), dim3(threads),
+                              params, shared_bytes, S(stream)));
+  return OMPRT_OK;
+}
+
 }  // extern "C"

@@ -15,9 +15,18 @@ sequential fallback when it returns 1.  `install()` points that name at
      own marshalling (_pack_arg / _write_back, host.py:209-230) and status
      contract (0 ran, 1 not runnable here → forge's fallback, 2 trap).
 
-Regions of any other shape return 1, exactly as an unsupported device would
-in the reference, and forge executes them on its host fallback.  forge is
-imported lazily from the calling process; the product package never needs it.
+Every other region runs as a compiled B200 image: the
+region's `nvptx64` IR image — forge's own codegen output, whose intrinsic
+table selectors.py:84-93 names the NVIDIA primitives — is translated to
+sm_100a by `regionc` and launched by `regions` (team = CTA, thread = CTA
+thread, vgpu semantics and trap messages).  Images come from, in order: a
+"b200" entry of the bundle (a precompiled cubin, `compile_bundle`), an
+"nvptx64" IR entry, or the program's own source module (stashed when the
+bridge is installed).  Only a region with no image at all returns 1 — the
+reference's "no runnable image" status — and forge then runs its fallback.
+
+forge is imported lazily from the calling process; the product package never
+needs it.
 """
 
 from __future__ import annotations
@@ -27,9 +36,11 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import runtime
+from . import regionc, regions, runtime
 
 DEVICE = "b200"
+IR_SOURCE_ARCH = "nvptx64"    # the forge image the B200 backend translates
+FAST_PATH = True              # recognised reductions -> the tuned omprt_reduce construct
 _NP = {"i32": np.int32, "u32": np.uint32, "i64": np.int64, "u64": np.uint64}
 _BITS = {"i32": 32, "u32": 32, "i64": 64, "u64": 64}
 
@@ -266,9 +277,11 @@ def _signed(v: int, elem: str) -> int:
 def b200_tgt_target(call, bundle, device="vgpu", force_fail: bool = False, *, grid=None,
                     sched_seed: int = 0, check_uninit: bool = False,
                     collect_trace: bool = False, out: dict | None = None) -> int:
-    """forge.host.tgt_target for device "b200" (other devices go to forge's own)."""
-    from forge import host as H
+    """forge.host.tgt_target for device "b200" (other devices go to forge's own).
 
+    Same contract as host.py:255-296: 0 ran on the device (buffers written
+    back), 1 not runnable here (caller runs the fallback), 2 trapped
+    (out["trap"] = (kind, detail); buffers untouched)."""
     arch = str(getattr(device, "arch", device))
     if arch != DEVICE:
         return _original(call, bundle, device, force_fail, grid=grid, sched_seed=sched_seed,
@@ -277,14 +290,28 @@ def b200_tgt_target(call, bundle, device="vgpu", force_fail: bool = False, *, gr
         raise ValueError("TargetCall is not bound to argument values")
     if force_fail or not torch.cuda.is_available():
         return 1
+    teams, threads = grid if grid is not None else (call.grid[0] or 1, call.grid[1] or 1)
+    if FAST_PATH and not check_uninit:
+        st = _run_recognised(call, teams, threads, out)
+        if st is not None:
+            return st
+    image = image_for(bundle, call)
+    if image is None or call.kernel_id not in image.kernels:
+        return 1
+    return _run_image(image, call, teams, threads, check_uninit, out)
+
+
+def _run_recognised(call, teams: int, threads: int, out: dict | None) -> int | None:
+    """The reduction idiom as one omprt_reduce construct launch, or None."""
+    from forge import host as H
+
     region = _region_of(call)
     if region is None:
-        return 1
+        return None
     try:
         plan = recognise(region)
     except Unrecognised:
-        return 1
-    teams, threads = grid if grid is not None else (call.grid[0] or 1, call.grid[1] or 1)
+        return None
     descs = {d.name: d for d in call.args}
     vals = dict(zip((d.name for d in call.args), call.values))
     scalars = {n: _signed(int(v), descs[n].elem.value) for n, v in vals.items()
@@ -295,33 +322,30 @@ def b200_tgt_target(call, bundle, device="vgpu", force_fail: bool = False, *, gr
         n = _eval(plan.nthreads, scalars, teams, threads)
         init = None if plan.init is None else _eval(plan.init, scalars, teams, threads)
     except Unrecognised:
-        return 1
+        return None
     # the device schedule partitions over every launched thread; a region
     # that names another thread count is a different partition
     if n != teams * threads or plan.cell not in descs or descs[plan.cell].elem.value != plan.elem:
-        return 1
+        return None
     if plan.op == "add" and init not in (None, 0):
-        return 1
+        return None
     dt = _NP[plan.elem]
     dev = torch.device("cuda", torch.cuda.current_device())
     cell_raw = bytearray(H._pack_arg(descs[plan.cell], vals[plan.cell]))
     cell = torch.from_numpy(np.frombuffer(cell_raw, dtype=dt).copy()).to(dev)
     if plan.src is None:
         if ub >= lb and (lb < 0 or ub > (1 << 40)):
-            return 1
+            return None
         m = (1 << _BITS[plan.elem]) - 1
         it = np.arange(0, max(ub + 1, 1), dtype=np.int64) & m
         x = torch.from_numpy(it.astype(np.uint64).astype(dt)).to(dev)
     else:
         if plan.src not in descs or descs[plan.src].elem.value != plan.elem:
-            return 1
+            return None
         raw = H._pack_arg(descs[plan.src], vals[plan.src])
         x = torch.from_numpy(np.frombuffer(raw, dtype=dt).copy()).to(dev)
         if ub >= lb and (lb < 0 or ub >= x.numel()):
-            if out is not None:
-                out["trap"] = ("OutOfBounds", f"iteration space [{lb}, {ub}] escapes "
-                               f"{plan.src}[0:{x.numel()}]")
-            return 2
+            return None  # the compiled image reproduces the vgpu's OutOfBounds trap
     out_dev = cell[:1]
     if init is not None and plan.op != "add":
         # an idempotent combine of the per-thread start value (max/min)
@@ -332,8 +356,160 @@ def b200_tgt_target(call, bundle, device="vgpu", force_fail: bool = False, *, gr
     torch.cuda.synchronize(dev)
     if out is not None:
         out["result"] = None
+        out["trace"] = []
     H._write_back(vals[plan.cell], cell.cpu().numpy().tobytes())
     return 0
+
+
+def _run_image(image, call, teams: int, threads: int, check_uninit: bool,
+               out: dict | None) -> int:
+    """tgt_target's marshalling (host.py:276-295) around regions.launch."""
+    from forge import host as H
+
+    packed: list[object] = []
+    for desc, v in zip(call.args, call.values):
+        if desc.kind == "scalar":
+            packed.append(int(v) & ((1 << desc.elem.bits) - 1))
+        else:
+            packed.append(bytearray(H._pack_arg(desc, v)))
+    res = regions.launch(image, call.kernel_id, (teams, threads), packed,
+                         check_uninit=check_uninit)
+    if out is not None:
+        out["trace"] = []
+        out["result"] = None
+    if res.status == "trap":
+        if out is not None:
+            out["trap"] = (res.trap, res.trap_detail)
+        return 2
+    for desc, v, raw in zip(call.args, call.values, res.buffers):
+        if desc.kind == "buffer":
+            H._write_back(v, raw)
+    return 0
+
+
+# ------------------------------------------------------------------ images
+
+def image_for(bundle, call=None):
+    """The B200 image for an offload: the bundle's "b200" entry, else its
+    "nvptx64" IR image compiled now, else the calling program's source module
+    compiled now (host._image_for, host.py:233-252, for the B200)."""
+    img = None
+    entries = None
+    if isinstance(bundle, dict):
+        entries = bundle
+    elif bundle is not None:
+        from forge.bundler import Bundle
+
+        b = bundle if isinstance(bundle, Bundle) else Bundle.from_bytes(bytes(bundle))
+        entries = dict(b.images)
+    if entries:
+        if DEVICE in entries:
+            e = entries[DEVICE]
+            img = e if isinstance(e, regionc.B200Image) else regionc.B200Image.from_bytes(e)
+        elif IR_SOURCE_ARCH in entries:
+            e = entries[IR_SOURCE_ARCH]
+            text = e.render() if hasattr(e, "render") else bytes(e).decode("utf-8")
+            img = regionc.compile_image(text)
+    if img is None and call is not None:
+        prog = _program_of(call)
+        mod = getattr(prog, "_b200_source", None) if prog is not None else None
+        if mod is not None:
+            img = getattr(prog, "_b200_image", None)
+            if img is None:
+                img = compile_module(mod)
+                prog._b200_image = img
+    return img
+
+
+def compile_module(module):
+    """forge SourceModule -> B200Image via forge's own nvptx64 device pipeline."""
+    import copy
+
+    from forge.codegen import compile_device_image
+    from forge.lowering import lower_atomics
+
+    lowered = lower_atomics(copy.deepcopy(module))
+    return regionc.compile_image(compile_device_image(lowered, IR_SOURCE_ARCH).render())
+
+
+def compile_source(source: str, filename: str = "<input>"):
+    from forge.parser import parse_module
+
+    return compile_module(parse_module(source, filename))
+
+
+def compile_bundle(source: str, targets=("vgpu", IR_SOURCE_ARCH, DEVICE),
+                   filename: str = "<input>") -> bytes:
+    """`forge compile --targets ...` with a "b200" entry: an OMPBNDL1 bundle
+    (bundler.py:37-98) whose "b200" payload is the sm_100a image of the
+    program's nvptx64 IR (SURVEY §8(f) #4)."""
+    import copy
+
+    from forge.bundler import bundle, host_payload
+    from forge.codegen import compile_device_image
+    from forge.host import emit_host_program
+    from forge.lowering import lower_atomics
+    from forge.parser import parse_module
+
+    module = parse_module(source, filename=filename)
+    lowered = lower_atomics(copy.deepcopy(module))
+    emit_host_program(lowered)
+    images = []
+    for arch in targets:
+        if arch == DEVICE:
+            ir = compile_device_image(copy.deepcopy(lowered), IR_SOURCE_ARCH).render()
+            images.append((DEVICE, regionc.compile_image(ir).to_bytes()))
+        else:
+            images.append((arch, compile_device_image(copy.deepcopy(lowered), arch)
+                           .render().encode("utf-8")))
+    return bundle(host_payload(source, filename=filename), images)
+
+
+def run_bundle(data, opts=None):
+    """forge.host.run_bundle (host.py:913-956) for device "b200": the images
+    handed to the host program are the bundle's own "b200" / "nvptx64"
+    entries (the reference loads images only for its runnable arch)."""
+    import json
+
+    from forge import host as H
+    from forge.bundler import Bundle, BundleError, HOST_ENTRY
+
+    opts = opts or H.RunOptions()
+    if opts.device != DEVICE:
+        return _original_run_bundle(data, opts)
+    try:
+        b = data if isinstance(data, Bundle) else Bundle.from_bytes(bytes(data))
+    except BundleError as err:
+        return H.HostRunResult("", f"error: {err}\n", 1, {}, [], [])
+    try:
+        payload = json.loads(b.host.decode("utf-8"))
+        source = payload["source"]
+        entry = opts.entry or payload.get("entry", "main")
+        filename = payload.get("filename", "<bundle>")
+    except (ValueError, KeyError, UnicodeDecodeError):
+        return H.HostRunResult("", f"error: malformed '{HOST_ENTRY}' payload in "
+                                   f"bundle\n", 1, {}, [], [])
+    from forge.diagnostics import CompileError
+    from forge.parser import parse_module
+
+    try:
+        module = parse_module(source, filename)
+        prog = H.HostProgram(module, entry=entry)
+        images = {}
+        for name, img in b.images:
+            if name == DEVICE:
+                images[DEVICE] = regionc.B200Image.from_bytes(img)
+            elif name == IR_SOURCE_ARCH and DEVICE not in dict(b.images):
+                images[DEVICE] = regionc.compile_image(img.decode("utf-8"))
+    except CompileError as err:
+        return H.HostRunResult("", f"{err}\n", 1, {}, [], [])
+    except (regionc.BadImage, regionc.RegionCompileError, UnicodeDecodeError) as err:
+        return H.HostRunResult("", f"error: bad device image in bundle: {err}\n",
+                               1, {}, [], [])
+    prog._b200_source = None  # a bundle without a device entry has no image
+    return prog.run(images, device=DEVICE, sched_seed=opts.sched_seed,
+                    force_offload_fail=opts.force_fail, check_uninit=opts.check_uninit,
+                    grid=opts.grid or (1, 1), collect_trace=opts.collect_trace)
 
 
 def runtime_fold(op: str, a: int, b: int, elem: str) -> int:
@@ -349,21 +525,122 @@ def _region_of(call):
     return None
 
 
+def _program_of(call):
+    fb = getattr(call, "fallback", None)
+    for cell in getattr(fb, "__closure__", None) or ():
+        try:
+            obj = cell.cell_contents
+        except ValueError:
+            continue
+        if type(obj).__name__ == "HostProgram":
+            return obj
+    return None
+
+
 _original = None
+_original_run_bundle = None
+_original_init = None
 
 
 def install() -> None:
-    """Route forge's offloads for device "b200" through the B200 path."""
-    global _original
+    """Route forge's offloads for device "b200" through the B200 path.
+
+    Patches forge.host.tgt_target (the `_RUNNABLE_ARCH` plug-in point,
+    host.py:62, 270), forge.host.run_bundle (bundles with b200/nvptx64
+    entries) and HostProgram.__init__ (keeps the program's source module so a
+    region without a bundled image is compiled on first offload, as
+    run_source compiles the image of its device, host.py:959-975)."""
+    global _original, _original_run_bundle, _original_init
     from forge import host as H
 
     if _original is None:
         _original = H.tgt_target
+        _original_run_bundle = H.run_bundle
+        _original_init = H.HostProgram.__init__
+
+        def __init__(self, module, entry="main"):
+            import copy
+
+            _original_init(self, module, entry)
+            self._b200_source = copy.deepcopy(module)
+
+        H.HostProgram.__init__ = __init__
     H.tgt_target = b200_tgt_target
+    H.run_bundle = run_bundle
 
 
 def uninstall() -> None:
+    global _original, _original_run_bundle, _original_init
     from forge import host as H
 
     if _original is not None:
         H.tgt_target = _original
+        H.run_bundle = _original_run_bundle
+        H.HostProgram.__init__ = _original_init
+        _original = _original_run_bundle = _original_init = None
+
+
+# ------------------------------------------------------------------ CLI
+
+def main(argv=None) -> int:
+    """`python -m paper_2106_03219_b200.forge_bridge compile|run|inspect ...`:
+    forge's CLI (cli.py:236-297) with "b200" as a target and a device."""
+    import argparse
+    import sys
+    from pathlib import Path
+
+    p = argparse.ArgumentParser(prog="forge-b200")
+    sub = p.add_subparsers(dest="cmd", required=True)
+    c = sub.add_parser("compile")
+    c.add_argument("input")
+    c.add_argument("--targets", default=f"vgpu,{IR_SOURCE_ARCH},{DEVICE}")
+    c.add_argument("-o", "--output")
+    r = sub.add_parser("run")
+    r.add_argument("bundle")
+    r.add_argument("--device", default=DEVICE)
+    r.add_argument("--sched-seed", type=int, default=0)
+    r.add_argument("--force-offload-fail", action="store_true")
+    r.add_argument("--check-uninit", action="store_true")
+    r.add_argument("--grid", metavar="TxN")
+    i = sub.add_parser("inspect")
+    i.add_argument("bundle")
+    a = p.parse_args(argv)
+    from forge import host as H
+
+    if a.cmd == "compile":
+        src = Path(a.input).read_text()
+        data = compile_bundle(src, tuple(t for t in a.targets.split(",") if t),
+                              filename=str(a.input))
+        Path(a.output or Path(a.input).with_suffix(".o")).write_bytes(data)
+        return 0
+    if a.cmd == "inspect":
+        from forge.bundler import Bundle
+
+        b = Bundle.from_bytes(Path(a.bundle).read_bytes())
+        for name, payload in b.entries:
+            extra = ""
+            if name == DEVICE:
+                img = regionc.B200Image.from_bytes(payload)
+                extra = (f"  [{img.manifest['arch']} cubin {len(img.cubin)} B, kernels "
+                         f"{', '.join(sorted(img.kernels))}]")
+            print(f"{name}\t{len(payload)}{extra}")
+        return 0
+    grid = None
+    if a.grid:
+        t, _, n = a.grid.partition("x")
+        grid = (int(t), int(n))
+    install()
+    try:
+        res = H.run_bundle(Path(a.bundle).read_bytes(),
+                           H.RunOptions(device=a.device, grid=grid,
+                                        force_fail=a.force_offload_fail,
+                                        sched_seed=a.sched_seed, check_uninit=a.check_uninit))
+    finally:
+        uninstall()
+    sys.stdout.write(res.stdout)
+    sys.stderr.write(res.stderr)
+    return res.exit_status
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

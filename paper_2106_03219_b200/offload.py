@@ -5,7 +5,9 @@ TargetCall), :255-296 (tgt_target) and vgpu.py:28-61 (TrapKind, TRAP_CODES,
 GridConfig).  Where the reference interprets a vgpu IR image, the B200 image
 is a table from kernel id (`__omp_offload_<region_id>`, codegen.py:59-63) to
 a RegionKernel naming the hand-written construct kernel that implements the
-region and which captured argument plays which role.
+region and which captured argument plays which role — or a compiled image
+(`regionc.B200Image`, the region's own IR translated to sm_100a), in which
+case every OpenMP thread runs the region literally (regions.launch).
 
 Status codes are the reference's: 0 ran on the device (buffers hold the
 results), 1 could not launch (force_fail, foreign arch, no image for the
@@ -23,7 +25,7 @@ from enum import Enum
 import numpy as np
 import torch
 
-from . import _lib, runtime
+from . import _lib, regionc, regions, runtime
 
 #: Arch names this device answers to: its own, and the reference's NVIDIA
 #: target whose intrinsic table (selectors.py:84-93) it implements.
@@ -214,6 +216,10 @@ def tgt_target(call: TargetCall, bundle, device="b200", force_fail: bool = False
     if force_fail or arch not in ARCHS:
         return 1
     image = _image_for(bundle, arch)
+    if isinstance(image, (bytes, bytearray)) and bytes(image[:8]) == regionc.IMAGE_MAGIC:
+        image = regionc.B200Image.from_bytes(image)
+    if isinstance(image, regionc.B200Image):
+        return _launch_compiled(image, call, grid, check_uninit, out)
     if image is None or call.kernel_id not in image:
         return 1
     rk: RegionKernel = image[call.kernel_id]
@@ -278,6 +284,32 @@ def tgt_target(call: TargetCall, bundle, device="b200", force_fail: bool = False
     for name, (d, v) in by_name.items():
         if d.kind == "buffer":
             _write_back(d, v, dbufs[name])
+    return 0
+
+
+def _launch_compiled(image, call: TargetCall, grid, check_uninit: bool, out) -> int:
+    """A compiled region (regionc.B200Image, from the reference's IR image):
+    every OpenMP thread runs the region literally on the B200 (regions.launch)."""
+    if call.kernel_id not in image.kernels:
+        return 1
+    teams, threads = grid if grid is not None else (call.grid[0] or 1, call.grid[1] or 1)
+    packed = []
+    for d, v in zip(call.args, call.values):
+        if d.kind == "scalar":
+            packed.append(int(v) & ((1 << ELEM_BITS[d.elem]) - 1))
+        else:
+            packed.append(bytearray(np.ascontiguousarray(_host_array(d, v)).tobytes()))
+    res = regions.launch(image, call.kernel_id, (teams, threads), packed,
+                         check_uninit=check_uninit)
+    if out is not None:
+        out["result"] = res
+    if res.status == "trap":
+        if out is not None:
+            out["trap"] = (res.trap, res.trap_detail)
+        return 2
+    for d, v, raw in zip(call.args, call.values, res.buffers):
+        if d.kind == "buffer":
+            _write_back(d, v, torch.frombuffer(bytearray(raw), dtype=torch.uint8))
     return 0
 
 

@@ -106,8 +106,10 @@ def test_forge_corpus_runs_on_b200(cuda):
             got = run_source(src, device="b200")
             assert got.stdout == want.stdout, name
             assert got.exit_status == want.exit_status == 0
+            # recognised reductions run as the omprt_reduce construct, every
+            # other region as its compiled sm_100a image: nothing falls back
             statuses = {s for _, s in got.offloads}
-            assert statuses == ({0} if name in RECOGNISED else {1}), (name, got.offloads)
+            assert statuses == {0}, (name, got.offloads)
     finally:
         B.uninstall()
 

@@ -1,0 +1,252 @@
+"""Compiled target regions on the B200 vs the reference's vgpu (GPU).
+
+Every program of tests/golden/region_programs.json (the vgpu's stdout,
+stderr with the trap message, exit status — recorded from the reference by
+oracle/gen_region_golden.py) is run by forge's own host program with device
+"b200": each offload region executes as its sm_100a image (regionc +
+regions), one CTA per team.  Results must be identical, trap messages
+included.  The recognised reduction idiom is forced through the image path
+too (FAST_PATH off), and the vgpu goldens of the generic-mode arena pattern,
+the check_uninit arena reads and the atomic-probe histories
+(tests/golden/fallback_runs.json) are re-run through compiled images.
+"""
+
+from __future__ import annotations
+
+import json
+import re
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+for cand in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+    if (cand / "forge" / "__init__.py").exists():
+        sys.path.insert(0, str(cand))
+        break
+forge = pytest.importorskip("forge")
+
+from forge import corpus  # noqa: E402
+from forge.host import HostProgram, RunOptions, run_source  # noqa: E402
+from forge.parser import parse_module  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+from paper_2106_03219_b200 import forge_bridge as B  # noqa: E402
+from paper_2106_03219_b200 import regions  # noqa: E402
+from tests.helpers import KIND, linearizable_programs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = json.loads((ROOT / "tests" / "golden" / "region_programs.json").read_text())
+
+
+@pytest.fixture
+def bridge(cuda):
+    B.install()
+    yield B
+    B.uninstall()
+    B.FAST_PATH = True
+
+
+@pytest.mark.parametrize("fast", [True, False])
+def test_golden_programs_match_vgpu(bridge, fast):
+    B.FAST_PATH = fast
+    for p in GOLDEN["programs"]:
+        got = run_source(p["source"], device="b200", **p["kwargs"])
+        assert (got.stdout, got.stderr, got.exit_status) == \
+            (p["stdout"], p["stderr"], p["exit_status"]), p["name"]
+        # every region ran on the device (0) or trapped there (2): nothing fell back
+        assert [list(x) for x in got.offloads] == p["offloads"], p["name"]
+        assert all(s in (0, 2) for _, s in got.offloads), p["name"]
+
+
+def test_bundles_run_their_b200_entry(bridge):
+    for p in GOLDEN["programs"][:6] + GOLDEN["programs"][-10:]:
+        data = B.compile_bundle(p["source"])
+        got = forge.host.run_bundle(data, RunOptions(device="b200",
+                                                     check_uninit=p["kwargs"].get("check_uninit",
+                                                                                  False)))
+        assert (got.stdout, got.stderr, got.exit_status) == \
+            (p["stdout"], p["stderr"], p["exit_status"]), p["name"]
+    # a bundle with only the nvptx64 IR image is compiled on load
+    p = GOLDEN["programs"][2]
+    data = B.compile_bundle(p["source"], targets=("nvptx64",))
+    got = forge.host.run_bundle(data, RunOptions(device="b200"))
+    assert got.stdout == p["stdout"] and all(s == 0 for _, s in got.offloads)
+    # no device entry at all: status 1 and forge's fallback, like the reference
+    data = B.compile_bundle(p["source"], targets=("vgpu",))
+    got = forge.host.run_bundle(data, RunOptions(device="b200"))
+    assert got.stdout == p["stdout"] and all(s == 1 for _, s in got.offloads)
+
+
+def test_cli_run(tmp_path, capsys, cuda):
+    p = next(q for q in GOLDEN["programs"] if q["name"] == "grid_map")
+    src = tmp_path / "g.mc"
+    src.write_text(p["source"])
+    assert B.main(["compile", str(src), "--targets", "b200"]) == 0
+    capsys.readouterr()
+    assert B.main(["run", str(tmp_path / "g.o")]) == 0
+    assert capsys.readouterr().out == p["stdout"]
+
+
+def test_corpus_through_images_matches_vgpu(bridge):
+    B.FAST_PATH = False
+    for name, src in corpus.CORPUS:
+        want = run_source(src, device="vgpu", sched_seed=1)
+        got = run_source(src, device="b200")
+        assert got.stdout == want.stdout and got.exit_status == 0, name
+        assert {s for _, s in got.offloads} == {0}, name
+
+
+def _call(src):
+    prog = HostProgram(parse_module(src))
+    return prog, prog.target_calls[0]
+
+
+def test_reduction_regions_through_images(bridge, fallback_golden):
+    from oracle.gen_golden import BODIES, REDUCE_SRC
+
+    import forge.host as H
+
+    B.FAST_PATH = False
+    for r in fallback_golden["reductions"]:
+        if r["n"] > 4096:
+            continue
+        body, atomic = BODIES[r["op"]]
+        src = REDUCE_SRC.format(T=r["dtype"], BODY=body.replace("{{", "{").replace("}}", "}"),
+                                ATOMIC=atomic)
+        prog, call = _call(src)
+        dt = {"i32": O.I32, "u32": O.U32, "i64": O.I64, "u64": O.U64}[r["dtype"]]
+        x = bytearray(O.fill(r["n"], dt, r["seed"], r["k"]).tobytes())
+        cell = bytearray(np.array([r["init"]], dtype=O.NP_DTYPE[dt]).tobytes())
+        vals = [{"x": x, "cell": cell, "n": r["n"]}[a.name] for a in call.args]
+        sink = {}
+        st = H.tgt_target(call.bind(vals), {}, "b200", grid=(r["teams"], r["threads"]), out=sink)
+        assert st == 0, sink
+        got = np.frombuffer(bytes(cell), dtype=O.NP_DTYPE[dt])[0]
+        assert int(got) == r["fallback"], r
+
+
+def test_generic_mode_pattern_matches_vgpu(bridge, fallback_golden):
+    """The SURVEY §A.7 globalisation program (tid 0 allocates from the arena,
+    barriers, per-thread partials in __shared_arena, ordered fold, LIFO free)
+    compiled whole: the arena is the image's team-shared __shared_arena."""
+    from oracle.gen_golden import GENERIC_SRC
+
+    import forge.host as H
+
+    for r in fallback_golden["generic"]:
+        prog, call = _call(GENERIC_SRC)
+        xs = O.fill(r["n"], O.I64, r["seed"], r["k"])
+        cell = bytearray(np.zeros(1, np.int64).tobytes())
+        offs = bytearray(np.full(r["teams"], -1, np.int64).tobytes())
+        named = {"x": bytearray(xs.tobytes()), "cell": cell, "offs": offs, "n": r["n"],
+                 "pad": r["pad"]}
+        sink = {}
+        st = H.tgt_target(call.bind([named[a.name] for a in call.args]), {}, "b200",
+                          grid=(r["teams"], r["threads"]), check_uninit=True, out=sink)
+        assert st == r["status"], (r, sink)
+        if st == 0:
+            assert int(np.frombuffer(bytes(cell), np.int64)[0]) == r["cell"]
+            assert np.frombuffer(bytes(offs), np.int64).tolist() == r["offsets"]
+        else:
+            # every team's thread 0 overflows; which team traps first is the
+            # interleaving's choice (vgpu: the seeded scheduler; here: the hardware)
+            kind, detail = sink["trap"]
+            assert kind == r["trap"][0]
+            assert re.sub(r"team \d+", "team T", detail) == re.sub(r"team \d+", "team T",
+                                                                   r["trap"][1])
+
+
+def test_uninit_arena_reads_match_vgpu(bridge, fallback_golden):
+    from oracle.gen_golden import UNINIT_SRC
+
+    import forge.host as H
+
+    for r in fallback_golden["uninit"]:
+        prog, call = _call(UNINIT_SRC)
+        buf = bytearray(16)
+        named = {"out": buf, "w": r["w"], "r": r["r"], "v": r["value"], "pad": r["pad"]}
+        sink = {}
+        st = H.tgt_target(call.bind([named[a.name] for a in call.args]), {}, "b200",
+                          grid=(2, 4), check_uninit=r["check"], out=sink)
+        assert st == r["status"], r
+        if st == 0:
+            read, off = np.frombuffer(bytes(buf), np.uint64).tolist()
+            assert (read, off) == (r["read"], r["off"]), r
+        else:
+            assert sink["trap"][0] == r["trap"]
+
+
+def test_atomic_program_probes_are_linearizable(bridge, fallback_golden):
+    import forge.host as H
+
+    for r in fallback_golden["program_probes"][::3]:
+        progs = [[tuple(op) for op in p] for p in r["programs"]]
+        src = corpus.probe_source(r["teams"], r["threads"], progs)
+        prog, call = _call(src)
+        total = sum(len(p) for p in progs)
+        cell = bytearray(4)
+        olds = bytearray(4 * total)
+        named = {"c": cell, "olds": olds}
+        st = H.tgt_target(call.bind([named[a.name] for a in call.args]), {}, "b200",
+                          grid=(r["teams"], r["threads"]))
+        assert st == 0
+        flat = np.frombuffer(bytes(olds), np.uint32).tolist()
+        per, k = [], 0
+        for p in progs:
+            per.append(flat[k:k + len(p)])
+            k += len(p)
+        final = int(np.frombuffer(bytes(cell), np.uint32)[0])
+        kinds = [[(KIND[k], e, d) for k, e, d in p] for p in progs]
+        assert linearizable_programs(O.U32, 0, kinds, per, final), r
+
+
+def test_launch_validation(cuda):
+    from paper_2106_03219_b200 import regionc as R
+
+    img = B.compile_source(GOLDEN["programs"][3]["source"])
+    with pytest.raises(ValueError):
+        regions.launch(img, "__omp_offload_9", (1, 1), [bytearray(16)])
+    with pytest.raises(ValueError):
+        regions.launch(img, "__omp_offload_0", (1, 1), [])
+    with pytest.raises(ValueError):
+        regions.launch(img, "__omp_offload_0", (0, 1), [bytearray(16)])
+    with pytest.raises(ValueError):
+        regions.launch(img, "__omp_offload_0", (1, 1), [5])
+    assert isinstance(img, R.B200Image)
+
+
+def test_large_grid_region(bridge):
+    """1024 teams x 1024 threads of a literal per-thread region (the vgpu's
+    grid limits, vgpu.py:56-60) — far beyond what the interpreter can run."""
+    import forge.host as H
+
+    src = """\
+u64 out[1048576];
+u64 cell[1];
+
+void kernel(u64 *out, u64 *cell) {
+  #pragma omp target
+  {
+    u64 g;
+    u64 old;
+    g = (u64) (omp_team_id() * omp_num_threads() + omp_thread_id());
+    out[g] = g * g;
+    old = __atomic_add(cell, g);
+  }
+}
+"""
+    prog, call = _call(src)
+    n = 1 << 20
+    out = bytearray(8 * n)
+    cell = bytearray(8)
+    named = {"out": out, "cell": cell}
+    st = H.tgt_target(call.bind([named[a.name] for a in call.args]), {}, "b200",
+                      grid=(1024, 1024))
+    assert st == 0
+    g = np.arange(n, dtype=np.uint64)
+    assert np.array_equal(np.frombuffer(bytes(out), np.uint64), g * g)
+    assert int(np.frombuffer(bytes(cell), np.uint64)[0]) == n * (n - 1) // 2
