@@ -132,7 +132,9 @@ int omprt_set_unroll(int unroll);
 
 /* Tuning knob (not part of the reference interface): kernel variant used by
  * the fp64 sum in SPMD mode — 0 default; 1-5 LDG load-policy / unroll
- * variants; 10-16 TMA bulk-copy (cp.async.bulk + mbarrier) stage rings. */
+ * variants; 10-16 TMA bulk-copy (cp.async.bulk + mbarrier) stage rings;
+ * 20 = ORDERED mode through the literal per-thread walk instead of the staged
+ * (cp.async shared-memory window) kernels. */
 int omprt_set_variant(int variant);
 
 /* Number of streaming multiprocessors of the current device (148 on B200). */

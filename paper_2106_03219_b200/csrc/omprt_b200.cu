@@ -1,6 +1,7 @@
 // omprt_b200.cu — the C ABI (include/omprt_b200.h) over the sm_100a kernels.
 // Single translation unit: the device runtime, every kernel and the host
 // entry points, so the trap word is one device symbol.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -11,6 +12,7 @@
 
 #include "bulk.cuh"
 #include "generic.cuh"
+#include "ordered.cuh"
 
 using namespace omprt;
 
@@ -44,6 +46,7 @@ inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int g_unroll = 4;   // tuning knob: vectors in flight per lane per iteration
 int g_variant = 0;  // tuning knob: kernel variant of the fp64 sum (0 = default)
+constexpr int kOrderedLiteral = 20;  // variant: ORDERED mode through the literal walk
 
 int check_grid(int teams, int threads) {
   if (teams < 1) return fail(OMPRT_EINVAL, "teams must be >= 1 (got %d)", teams);
@@ -111,18 +114,109 @@ int launch_variant(int v, const T *xp, LoopArgs la, int teams, int threads, Work
   return check_launch("omprt_reduce(variant)");
 }
 
+int sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return sms;
+}
+
+// ORDERED row-group kernels (ordered.cuh).  Each CTA = nw streaming warps +
+// the folder warp; one CTA per SM (the tile ring takes most of the shared
+// memory), never more CTAs than the warp groups need.  Every launch gets a
+// fresh epoch for the per-group ready flags (so the workspace is reused
+// without re-zeroing).
+std::atomic<uint32_t> g_ord_epoch{0};
+
+uint32_t next_epoch() {
+  uint32_t e = ++g_ord_epoch;
+  if (e == 0) e = ++g_ord_epoch;  // 0 is the zeroed workspace's value
+  return e;
+}
+
+inline int ord_grid(int teams, int threads, int nw) {
+  const int64_t groups = ((int64_t)teams * threads + 31) / 32;
+  int64_t g = (groups + nw - 1) / nw;
+  const int sms = sm_count();
+  if (sms > 0 && g > sms) g = sms;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// streaming warps per CTA: enough that every SM gets work, at most 8
+inline int ord_default_nw(int teams, int threads) {
+  const int64_t groups = ((int64_t)teams * threads + 31) / 32;
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  int64_t nw = (groups + sms - 1) / sms;
+  return (int)(nw < 1 ? 1 : (nw > 8 ? 8 : nw));
+}
+
+template <class T, int OP, int WB>
+int launch_ordered_rows(const T *xp, LoopArgs la, int teams, int threads, int nw, Workspace w,
+                        T *op, cudaStream_t st) {
+  constexpr int W = WB / (int)sizeof(T);
+  using L = OrdSmem<T, W, 1>;
+  const int stages = L::stages_for(nw);
+  if (stages < 2) return fail(OMPRT_EINVAL, "ordered rows: %d warps x %d B do not fit", nw, WB);
+  const size_t ring = (size_t)nw * L::warp_bytes(stages);
+  const size_t smem = ring + kFolderSmem;
+  auto kern = k_reduce_ordered_rows<T, OP, W>;
+  int rc = set_smem(kern, smem);
+  if (rc) return rc;
+  kern<<<ord_grid(teams, threads, nw), (nw + 1) * 32, smem, st>>>(
+      xp, la, teams, threads, w, op, stages, next_epoch(), (uint32_t)ring);
+  return check_launch("omprt_reduce(ordered rows)");
+}
+
+// Default ORDERED policy: 512-byte row windows when three stages fit, else
+// 256-byte windows.
+template <class T, int OP>
+int launch_ordered_default(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
+                           cudaStream_t st) {
+  const int nw = ord_default_nw(teams, threads);
+  if (OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(nw) >= 3)
+    return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, nw, w, op, st);
+  return launch_ordered_rows<T, OP, 256>(xp, la, teams, threads, nw, w, op, st);
+}
+
+// Tuning variants of the ORDERED fp64 sum (21..29): window bytes × warps.
+template <class T, int OP>
+int launch_ordered_variant(int v, const T *xp, LoopArgs la, int teams, int threads, Workspace w,
+                           T *op, cudaStream_t st) {
+  switch (v) {
+    case 21: return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 4, w, op, st);
+    case 22: return launch_ordered_rows<T, OP, 256>(xp, la, teams, threads, 8, w, op, st);
+    case 23: return launch_ordered_rows<T, OP, 128>(xp, la, teams, threads, 16, w, op, st);
+    case 24: return launch_ordered_rows<T, OP, 256>(xp, la, teams, threads, 4, w, op, st);
+    case 25: return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 2, w, op, st);
+    case 26: return launch_ordered_rows<T, OP, 256>(xp, la, teams, threads, 12, w, op, st);
+    case 27: return launch_ordered_rows<T, OP, 128>(xp, la, teams, threads, 8, w, op, st);
+    default: return fail(OMPRT_EINVAL, "unknown ordered variant %d", v);
+  }
+}
+
 template <class T, int OP>
 int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode, Workspace w,
                     void *out, cudaStream_t st) {
   const T *xp = (const T *)x;
   T *op = (T *)out;
   if constexpr (std::is_same<T, double>::value && OP == OMPRT_OP_ADD) {
-    if (g_variant != 0 && mode == OMPRT_MODE_SPMD)
+    if (g_variant != 0 && g_variant < kOrderedLiteral && mode == OMPRT_MODE_SPMD)
       return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
   }
   const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
   if (mode == OMPRT_MODE_ORDERED) {
-    k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
+    // staged per-thread windows (ordered.cuh); the literal walk for small
+    // chunks, partial warps, or variant kOrderedLiteral
+    if constexpr (std::is_same<T, double>::value && OP == OMPRT_OP_ADD) {
+      if (g_variant > kOrderedLiteral && g_variant < 30)
+        return launch_ordered_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
+    }
+    if (g_variant != kOrderedLiteral && ord_rows_ok(la, x)) {
+      return launch_ordered_default<T, OP>(xp, la, teams, threads, w, op, st);
+    } else {
+      k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
+    }
   } else if (bulk_ok) {
     // default SPMD path: TMA bulk-copy stage ring
     return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, threads, w, op, st);
@@ -436,7 +530,35 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
   Workspace w = ws_carve(d_ws, teams, 2);
   const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
   if (mode == OMPRT_MODE_ORDERED) {
-    k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+    if (g_variant != kOrderedLiteral && ord_rows_ok(la, d_x, d_y)) {
+      const int nw = ord_default_nw(teams, threads);
+      const int s512 = OrdSmem<double, 64, 2>::stages_for(nw);
+      const int s256 = OrdSmem<double, 32, 2>::stages_for(nw);
+      const int s128 = OrdSmem<double, 16, 2>::stages_for(nw);
+      const int grid = ord_grid(teams, threads, nw);
+      const uint32_t ep = next_epoch();
+      if (s512 >= 3) {
+        const size_t ring = (size_t)nw * OrdSmem<double, 64, 2>::warp_bytes(s512);
+        const size_t smem = ring + kFolderSmem;
+        if ((rc = set_smem(k_dot_ordered_rows<64>, smem))) return rc;
+        k_dot_ordered_rows<64><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
+            d_x, d_y, la, teams, threads, w, d_out, s512, ep, (uint32_t)ring);
+      } else if (s256 >= 2) {
+        const size_t ring = (size_t)nw * OrdSmem<double, 32, 2>::warp_bytes(s256);
+        const size_t smem = ring + kFolderSmem;
+        if ((rc = set_smem(k_dot_ordered_rows<32>, smem))) return rc;
+        k_dot_ordered_rows<32><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
+            d_x, d_y, la, teams, threads, w, d_out, s256, ep, (uint32_t)ring);
+      } else {
+        const size_t ring = (size_t)nw * OrdSmem<double, 16, 2>::warp_bytes(s128);
+        const size_t smem = ring + kFolderSmem;
+        if ((rc = set_smem(k_dot_ordered_rows<16>, smem))) return rc;
+        k_dot_ordered_rows<16><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
+            d_x, d_y, la, teams, threads, w, d_out, s128, ep, (uint32_t)ring);
+      }
+    } else {
+      k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+    }
   } else if (bulk_ok) {
     auto kern = k_dot_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;

@@ -1,0 +1,446 @@
+// ordered.cuh — ORDERED mode at streaming speed.  Every OpenMP thread still
+// folds exactly its own schedule chunks in iteration order (the host
+// fallback's per-thread loop, host.py:567-582) and the per-thread partials
+// are combined in global thread order, so fp results are bit-identical to
+// the reference order; only the way the bytes reach the fold changes.
+//
+// Why not the literal walk (k_reduce_ordered, kernels.cuh): its lane l reads
+// row l (its own block) one element at a time, so DRAM sees thousands of
+// rows advancing in 32-byte sectors; and staging 32 rows × W elements for
+// every resident warp runs out of shared memory before the row pieces get
+// long enough for HBM (measured: 128-byte pieces 3.4 TB/s, 256-byte pieces
+// 4.3 TB/s — profiles/r1_ordered_sweep.jsonl).
+//
+// Row-group design: the CUDA grid is decoupled from the OpenMP geometry.  The
+// P = teams × threads OpenMP threads are cut into groups of 32 consecutive
+// global thread ids; each CUDA warp takes groups round-robin, one lane per
+// OpenMP thread (lane l plays thread g·32+l: its (team, tid) gives its
+// schedule_init bounds).  Per group the warp streams W-element windows of
+// its 32 rows through a ring of STAGES shared-memory tiles with 16-byte
+// cp.async copies (SASS LDGSTS.128; each warp instruction moves 32 × 16 B
+// of row pieces W·sizeof(T) bytes long), and lane l folds row l of each tile
+// in order out of shared memory (row stride = U+1 16-byte units, an odd
+// number, so the lanes' 16-byte reads are bank-conflict-free).  Only NW × 32
+// rows per SM are in flight, so pieces can be ≥ 512 B while the ring still
+// fits in shared memory.  Windows are aligned to 16 bytes in the address
+// space and never cross a schedule chunk; window elements outside the row
+// are copied (outside [lb, ub]: skipped) but never folded.  All P
+// partials are combined in global thread order.  The folding of the partials (a strictly
+// sequential chain) is done by one extra "folder" warp that follows the
+// streaming warps group by group (per-group ready flags), overlapping it with
+// the stream.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace omprt {
+
+constexpr int kOrdSmemBudget = 216 * 1024;  // dynamic smem of a CTA's streaming warps
+
+OMPRT_D void cp_async_16(void *smem_dst, const void *gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(d), "l"(gsrc)
+               : "memory");
+}
+
+template <int BYTES> OMPRT_D void cp_async_small(void *smem_dst, const void *gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  if (BYTES == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+OMPRT_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+// wait until at most `pending` groups of this thread are outstanding
+OMPRT_D void cp_async_wait(int pending) {
+  switch (pending) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+  }
+}
+
+OMPRT_D void st_release_gpu(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+OMPRT_D uint32_t ld_acquire_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+constexpr int kOrdMaxStages = 6;
+
+// One OpenMP thread's walk over its schedule chunks (run_thread_chunks,
+// loops.cuh), in W-element windows aligned to V elements (16 bytes).
+template <int W, int V> struct OrdRow {
+  int64_t p;   // next element to fold (current chunk)
+  int64_t hi;  // current chunk end (inclusive)
+  int64_t a;   // current window start (V-aligned, a <= p)
+  int64_t clo, stride, limit, chunk;
+  bool chunked;
+
+  OMPRT_D void init(const LoopArgs &la, int64_t g, int64_t teams, int64_t threads) {
+    chunked = (la.sched == OMPRT_SCHED_STATIC_CHUNKED ||
+               la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED);
+    if (g >= teams * threads) {  // lane past the last OpenMP thread: dead row
+      p = 1;
+      hi = 0;
+      a = 0;
+      chunked = false;
+      return;
+    }
+    const Bounds bd = schedule_init(la.sched, la.lb, la.ub, la.chunk, g / threads, teams,
+                                    g % threads, threads);
+    stride = bd.stride;
+    limit = bd.limit;
+    chunk = la.chunk;
+    clo = bd.lower;
+    p = bd.lower;
+    if (chunked) {
+      hi = (bd.lower <= bd.limit) ? bd.lower + chunk - 1 : bd.lower - 1;
+      if (hi > bd.limit) hi = bd.limit;
+    } else {
+      hi = bd.upper;
+    }
+    a = p & ~(int64_t)(V - 1);
+  }
+  OMPRT_D bool live() const { return p <= hi; }
+  // the current window's fold range as offsets from a: [s, e]
+  OMPRT_D int s() const { return (int)(p - a); }
+  OMPRT_D int e() const { return (int)((hi - a) < (W - 1) ? (hi - a) : (W - 1)); }
+  OMPRT_D void advance() {
+    a += W;
+    p = a;
+    if (p > hi && chunked) {
+      clo += stride;
+      if (clo <= limit) {
+        p = clo;
+        hi = clo + chunk - 1;
+        if (hi > limit) hi = limit;
+        a = p & ~(int64_t)(V - 1);
+      }
+    }
+  }
+};
+
+// Shared-memory picture of one warp: table[32] {a, e or -1 if the row is
+// done} of the window being issued | STAGES × NS tiles of 32 rows ×
+// (U+1) 16-byte units.
+template <class T, int W, int NS> struct OrdSmem {
+  static constexpr int V = 16 / (int)sizeof(T);
+  static constexpr int U = W / V;         // 16-byte units per row window
+  static constexpr int RS = (U + 1) * V;  // row stride in elements (odd # of units)
+  static constexpr size_t kTile = (size_t)32 * RS * sizeof(T);
+  static constexpr size_t kTable = 32 * sizeof(longlong2);
+  OMPRT_HD static size_t warp_bytes(int stages) { return kTable + (size_t)stages * NS * kTile; }
+  // stages for nw warps per CTA within the budget (0 = does not fit)
+  OMPRT_HD static int stages_for(int nw) {
+    for (int s = kOrdMaxStages; s >= 2; --s)
+      if ((size_t)nw * warp_bytes(s) <= (size_t)kOrdSmemBudget) return s;
+    return 0;
+  }
+};
+
+// Issue the cp.async copies of every live row's current window of this
+// warp's group into stage `st` (one commit group), then advance this lane's
+// load cursor.  All 32 lanes call it.  Copy f = i·32 + lane of the window
+// is unit j = f % U of row r = f / U (U a power of two: shifts), so each
+// warp instruction covers whole 16-byte-aligned row pieces.  Windows that
+// touch lb or ub (the first/last of the iteration space) take the
+// element-checked path; everything else is one table read + one LDGSTS.128.
+template <class T, int W, int NS>
+OMPRT_D void ord_issue(OrdRow<W, 16 / sizeof(T)> &row, const T *const (&src)[NS], int64_t lb,
+                       int64_t ub, longlong2 *table, T *tiles, int st, uint32_t lane) {
+  using L = OrdSmem<T, W, NS>;
+  constexpr int V = L::V, U = L::U;
+  static_assert((U & (U - 1)) == 0, "units per window must be a power of two");
+  const bool live = row.live();
+  const bool inside = !live || (row.a >= lb && row.a + W - 1 <= ub);
+  table[lane] = make_longlong2(row.a, live ? (long long)row.e() : -1ll);
+  const bool fast = __all_sync(0xffffffffu, inside);
+  __syncwarp();  // table writes visible to the warp
+  T *tile0 = tiles + (size_t)st * NS * (L::kTile / sizeof(T));
+  if (fast) {
+#pragma unroll 8
+    for (int i = 0; i < U; ++i) {
+      const int f = i * 32 + (int)lane;
+      const int r = f / U, j = f % U;
+      const longlong2 en = table[r];
+      if (j * V <= (int)en.y) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          cp_async_16(tile0 + (size_t)s * (L::kTile / sizeof(T)) + r * L::RS + j * V,
+                      src[s] + en.x + j * V);
+      }
+    }
+  } else {
+    for (int i = 0; i < U; ++i) {
+      const int f = i * 32 + (int)lane;
+      const int r = f / U, j = f % U;
+      const longlong2 en = table[r];
+      if (j * V <= (int)en.y) {
+        const int64_t e0 = en.x + (int64_t)j * V;
+        for (int s = 0; s < NS; ++s) {
+          T *dst = tile0 + (size_t)s * (L::kTile / sizeof(T)) + r * L::RS + j * V;
+          if (e0 >= lb && e0 + V - 1 <= ub) {
+            cp_async_16(dst, src[s] + e0);
+          } else {
+            for (int k = 0; k < V; ++k)
+              if (e0 + k >= lb && e0 + k <= ub)
+                cp_async_small<sizeof(T)>(dst + k, src[s] + e0 + k);
+          }
+        }
+      }
+    }
+  }
+  cp_async_commit();
+  __syncwarp();
+  if (live) row.advance();
+}
+
+// Stream this warp's groups through the ring; fold(rows, s, e) consumes this
+// lane's row offsets s..e of the current tile in order, fold.publish(g)
+// stores OpenMP thread g's partial; then flags[grp] = epoch announces the
+// group's 32 partials to the folder.
+template <class T, int W, int NS, class Fold>
+OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
+                        const T *const (&src)[NS], int stages, Fold &fold, uint32_t *flags,
+                        uint32_t epoch) {
+  using L = OrdSmem<T, W, NS>;
+  constexpr int V = L::V;
+  extern __shared__ __align__(16) unsigned char ord_smem[];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t nwarps = (blockDim.x >> 5) - 1;  // the last warp is the folder's
+  unsigned char *base = ord_smem + (size_t)warp * L::warp_bytes(stages);
+  longlong2 *table = (longlong2 *)base;
+  T *tiles = (T *)(base + L::kTable);
+  const int64_t P = teams * threads;
+  const int64_t ngroups = (P + 31) / 32;
+  for (int64_t grp = (int64_t)blockIdx.x * nwarps + warp; grp < ngroups;
+       grp += (int64_t)gridDim.x * nwarps) {
+    OrdRow<W, V> ld, fd;
+    ld.init(la, grp * 32 + lane, teams, threads);
+    fd = ld;
+    for (int s = 0; s + 1 < stages; ++s)
+      ord_issue<T, W, NS>(ld, src, la.lb, la.ub, table, tiles, s, lane);
+    for (int t = 0;; ++t) {
+      if (!__any_sync(0xffffffffu, fd.live())) break;
+      ord_issue<T, W, NS>(ld, src, la.lb, la.ub, table, tiles, (t + stages - 1) % stages, lane);
+      cp_async_wait(stages - 1);
+      __syncwarp();
+      if (fd.live()) {
+        const int st = t % stages;
+        const T *rows[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          rows[s] = tiles + (size_t)(st * NS + s) * (L::kTile / sizeof(T)) + lane * L::RS;
+        fold(rows, fd.s(), fd.e());
+        fd.advance();
+      }
+      __syncwarp();
+    }
+    cp_async_wait(0);
+    __syncwarp();
+    if (grp * 32 + lane < P) fold.publish(grp * 32 + lane);
+    // group ready: the lanes' partials, then the flag (release, gpu scope)
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_gpu(flags + grp, epoch);
+  }
+}
+
+// Load V elements (16 bytes) of a shared-memory row.
+template <class T, int V> OMPRT_D void lds_vec(T (&v)[V], const T *p) {
+  const uint4 q = *reinterpret_cast<const uint4 *>(p);
+  memcpy(v, &q, 16);
+}
+
+// One row's in-order fold of a window: offsets s..e of `row`.
+template <class T, int OP, int W> struct OrdReduceFold {
+  static constexpr int V = 16 / (int)sizeof(T);
+  T part;
+  T *tp;
+  OMPRT_D void operator()(const T *const (&rows)[1], int s, int e) {
+    const T *r = rows[0];
+    if (s == 0 && e == W - 1) {
+#pragma unroll 4
+      for (int q = 0; q < W / V; ++q) {
+        T v[V];
+        lds_vec<T, V>(v, r + q * V);
+#pragma unroll
+        for (int k = 0; k < V; ++k) part = Red<OP, T>::apply(part, v[k]);
+      }
+    } else {
+      for (int o = s; o <= e; ++o) part = Red<OP, T>::apply(part, r[o]);
+    }
+  }
+  OMPRT_D void publish(int64_t g) {
+    tp[g] = part;
+    part = Red<OP, T>::identity();
+  }
+};
+
+template <int W> struct OrdDotFold {
+  double part;
+  double *tp;
+  OMPRT_D void operator()(const double *const (&rows)[2], int s, int e) {
+    const double *a = rows[0], *b = rows[1];
+    if (s == 0 && e == W - 1) {
+#pragma unroll 4
+      for (int q = 0; q < W / 2; ++q) {
+        double va[2], vb[2];
+        lds_vec<double, 2>(va, a + 2 * q);
+        lds_vec<double, 2>(vb, b + 2 * q);
+        part = __fma_rn(va[0], vb[0], part);
+        part = __fma_rn(va[1], vb[1], part);
+      }
+    } else {
+      for (int o = s; o <= e; ++o) part = __fma_rn(a[o], b[o], part);
+    }
+  }
+  OMPRT_D void publish(int64_t g) {
+    tp[g] = part;
+    part = 0.0;
+  }
+};
+
+OMPRT_D uint32_t ld_relaxed_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The folder: one warp (the extra warp of CTA 0) folds the P per-thread
+// partials into *out strictly in global thread order — the fallback's
+// combine order (host.py:567-582) — following the streaming warps as their
+// group flags turn to this launch's epoch, so the sequential chain overlaps
+// the stream instead of trailing it.  Batches of kFoldB groups (256
+// partials): lane l waits (ld.acquire) for the flag of group l/4 of batch
+// b+2, loads its 8 partials into registers, and stores them into a 2-slot
+// shared-memory ring one iteration later; meanwhile the warp folds batch b
+// out of the ring with broadcast loads, one dependent add per partial (the
+// chain is the floor: ~8 cycles per fp64 add).
+constexpr int kFoldB = 8;                                 // groups per batch
+constexpr int kFoldPer = kFoldB * 32;                     // partials per batch
+constexpr size_t kFolderSmem = 2 * kFoldPer * 8;          // the ring (bytes)
+
+template <class T> struct FoldLoad {
+  static constexpr int N = kFoldPer / 32;  // partials per lane per batch
+  T v[N];
+};
+
+template <class T>
+OMPRT_D void ord_folder_load(const T *tp, int64_t P, const uint32_t *flags, uint32_t epoch,
+                             int64_t b, FoldLoad<T> &L) {
+  constexpr int N = FoldLoad<T>::N;
+  const uint32_t lane = threadIdx.x & 31u;
+  const int64_t first = b * kFoldPer + (int64_t)lane * N;  // this lane's partials
+  if (first < P) {
+    const int64_t grp = first / 32;
+    while (ld_acquire_gpu(flags + grp) != epoch) {
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) L.v[k] = (first + k < P) ? ld_cg(tp + first + k) : T();
+}
+
+template <int OP, class T, class Combine>
+OMPRT_D void ord_folder(const T *tp, int64_t P, const uint32_t *flags, uint32_t epoch, T *out,
+                        T *ring, Combine &&comb) {
+  constexpr int N = FoldLoad<T>::N;
+  const uint32_t lane = threadIdx.x & 31u;
+  const int64_t nb = (P + kFoldPer - 1) / kFoldPer;
+  T acc = *out;
+  FoldLoad<T> L;
+  ord_folder_load<T>(tp, P, flags, epoch, 0, L);
+#pragma unroll
+  for (int k = 0; k < N; ++k) ring[lane * N + k] = L.v[k];
+  if (nb > 1) ord_folder_load<T>(tp, P, flags, epoch, 1, L);
+  for (int64_t b = 0; b < nb; ++b) {
+    T *cur = ring + (b & 1) * kFoldPer;
+    T *nxt = ring + ((b + 1) & 1) * kFoldPer;
+    if (b + 1 < nb) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) nxt[lane * N + k] = L.v[k];
+    }
+    if (b + 2 < nb) ord_folder_load<T>(tp, P, flags, epoch, b + 2, L);
+    __syncwarp();
+    const int64_t base = b * kFoldPer;
+    if (base + kFoldPer <= P) {
+#pragma unroll 32
+      for (int j = 0; j < kFoldPer; ++j) acc = comb(acc, cur[j]);
+    } else {
+      for (int j = 0; base + j < P; ++j) acc = comb(acc, cur[j]);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) *out = acc;
+}
+
+template <int OP, class T> struct RedComb {
+  OMPRT_D T operator()(T a, T b) const { return Red<OP, T>::apply(a, b); }
+};
+
+// flags live after the P partials in the (2-slot) thread-partial area
+OMPRT_HD size_t ord_flags_offset(int64_t P) { return (size_t)P * 8; }
+
+constexpr int kOrdMaxWarps = 16;  // streaming warps per CTA (+1 folder warp)
+
+template <class T, int OP, int W>
+__global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
+    k_reduce_ordered_rows(const T *__restrict__ x, LoopArgs la, int teams, int threads,
+                          Workspace ws, T *out, int stages, uint32_t epoch, uint32_t ring_off) {
+  const int64_t P = (int64_t)teams * threads;
+  T *tp = (T *)ws.thread_partials;
+  uint32_t *flags = (uint32_t *)(ws.thread_partials + ord_flags_offset(P));
+  if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
+    extern __shared__ __align__(16) unsigned char ord_smem[];
+    if (blockIdx.x == 0)
+      ord_folder<OP, T>(tp, P, flags, epoch, out, (T *)(ord_smem + ring_off), RedComb<OP, T>());
+    return;
+  }
+  OrdReduceFold<T, OP, W> f{Red<OP, T>::identity(), tp};
+  const T *src[1] = {x};
+  ord_groups<T, W, 1>(la, teams, threads, src, stages, f, flags, epoch);
+}
+
+template <int W>
+__global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
+    k_dot_ordered_rows(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
+                       int teams, int threads, Workspace ws, double *out, int stages,
+                       uint32_t epoch, uint32_t ring_off) {
+  const int64_t P = (int64_t)teams * threads;
+  double *tp = (double *)ws.thread_partials;
+  uint32_t *flags = (uint32_t *)(ws.thread_partials + ord_flags_offset(P));
+  if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
+    extern __shared__ __align__(16) unsigned char ord_smem[];
+    if (blockIdx.x == 0)
+      ord_folder<OMPRT_OP_ADD, double>(tp, P, flags, epoch, out, (double *)(ord_smem + ring_off),
+                                       RedComb<OMPRT_OP_ADD, double>());
+    return;
+  }
+  OrdDotFold<W> f{0.0, tp};
+  const double *src[2] = {x, y};
+  ord_groups<double, W, 2>(la, teams, threads, src, stages, f, flags, epoch);
+}
+
+// Host side: can the row-group kernels take this launch?  x (and y) must be
+// 16-byte aligned; chunked schedules need chunk >= kOrdMinChunk (smaller
+// chunks keep the literal walk, which is coalesced across lanes for chunk 1).
+constexpr int64_t kOrdMinChunk = 16;
+
+__host__ inline bool ord_rows_ok(const LoopArgs &la, const void *x, const void *y = nullptr) {
+  if (((uintptr_t)x & 15) != 0 || ((uintptr_t)y & 15) != 0) return false;
+  const bool chunked = (la.sched == OMPRT_SCHED_STATIC_CHUNKED ||
+                        la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED);
+  return !chunked || la.chunk >= kOrdMinChunk;
+}
+
+}  // namespace omprt
