@@ -1,0 +1,126 @@
+"""ORDERED mode through the row-group kernels (csrc/ordered.cuh): every
+OpenMP thread's in-order fold and the global-thread-order combine must be
+bit-identical to the reference order (host.py:567-582) restated in
+oracle/omprt_oracle.c — for fp too — on every geometry: threads not a
+multiple of 32, groups straddling teams, windows touching lb/ub, chunked
+schedules on both sides of the row-kernel threshold, misaligned pointers
+(literal walk), and the full 2^30 C2 size."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2106_03219_b200 import runtime
+
+pytestmark = pytest.mark.gpu
+
+SCHEDS = {"static": O.STATIC, "static_chunked": O.STATIC_CHUNKED,
+          "distribute": O.DISTRIBUTE, "distribute_chunked": O.DISTRIBUTE_CHUNKED}
+DTS = {"f64": O.F64, "f32": O.F32, "i64": O.I64, "u32": O.U32}
+LITERAL = 20  # omprt_set_variant: ORDERED through the literal per-thread walk
+
+
+def _ordered(xd, op, sched, chunk, teams, threads, lb, ub, init):
+    out = torch.zeros(1, dtype=xd.dtype, device=xd.device)
+    out.fill_(init)
+    runtime.reduce(xd, op, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                   threads=threads, mode="ordered", out=out)
+    return out.cpu().numpy()[0]
+
+
+@pytest.mark.parametrize("dtype", list(DTS))
+def test_rows_kernel_bit_exact_random_geometries(cuda, dtype):
+    dt = DTS[dtype]
+    n = 400_009
+    x = O.fill(n, dt, O.SEED, 3)
+    xd = torch.from_numpy(x).to(cuda)
+    rng = np.random.default_rng(2106)
+    cases = [(3, 100, 0, n - 1, "static", 1), (148, 256, 1, n - 2, "distribute", 1),
+             (7, 33, 5, n - 7, "distribute", 1), (1, 1, 0, n - 1, "static", 1),
+             (2, 1000, 0, 12_345, "static", 1), (40, 64, 3, n - 1, "static_chunked", 16),
+             (9, 96, 0, n - 1, "distribute_chunked", 300), (5, 64, 0, n - 1, "static_chunked", 15)]
+    for _ in range(12):
+        sched = str(rng.choice(list(SCHEDS)))
+        lb = int(rng.integers(0, 50))
+        cases.append((int(rng.integers(1, 200)), int(rng.integers(1, 1025)), lb,
+                      int(rng.integers(lb - 3, n)), sched, int(rng.integers(1, 5000))))
+    for op in ("add", "max"):
+        init = 0 if op == "add" else (-np.inf if dt in (O.F32, O.F64)
+                                      else np.iinfo(O.NP_DTYPE[dt]).min)
+        for teams, threads, lb, ub, sched, chunk in cases:
+            opc = O.ADD if op == "add" else O.MAX
+            want = O.reduce(x, lb, ub, dt, opc, SCHEDS[sched], chunk, teams, threads, init)
+            got = _ordered(xd, op, sched, chunk, teams, threads, lb, ub, init)
+            assert np.array([got]).tobytes() == np.array([want], dtype=x.dtype).tobytes(), \
+                (dtype, op, teams, threads, lb, ub, sched, chunk, got, want)
+
+
+def test_rows_and_literal_agree(cuda):
+    n = 1_000_003
+    xd = runtime.synthetic(n, "f64", O.SEED, 4, device=cuda)
+    try:
+        for teams, threads, sched, chunk in ((148, 256, "distribute", 1), (13, 77, "static", 1),
+                                             (64, 512, "static_chunked", 100)):
+            rows = _ordered(xd, "add", sched, chunk, teams, threads, 0, n - 1, 0.0)
+            runtime.set_variant(LITERAL)
+            lit = _ordered(xd, "add", sched, chunk, teams, threads, 0, n - 1, 0.0)
+            runtime.set_variant(0)
+            assert rows == lit, (teams, threads, sched)
+    finally:
+        runtime.set_variant(0)
+
+
+def test_misaligned_pointer_falls_back_to_literal(cuda):
+    # an 8-byte offset view: the row kernels need 16-byte alignment, the
+    # literal walk takes it — same bits
+    n = 100_001
+    x = O.fill(n + 1, O.F64, O.SEED, 6)
+    base = torch.from_numpy(x).to(cuda)
+    view = base[1:]
+    assert view.data_ptr() % 16 == 8
+    want = O.reduce(np.ascontiguousarray(x[1:]), 0, n - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, 11, 64)
+    assert _ordered(view, "add", "distribute", 1, 11, 64, 0, n - 1, 0.0) == want
+
+
+def test_dot_ordered_rows_bit_exact(cuda):
+    n = 700_001
+    x, y = O.fill(n, O.F64, O.SEED, 0), O.fill(n, O.F64, O.SEED, 1)
+    xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+    for teams, threads, lb, ub, sched, chunk in ((148, 256, 0, n - 1, "distribute", 1),
+                                                 (9, 40, 3, n - 2, "static", 1),
+                                                 (20, 128, 0, n - 1, "static_chunked", 64)):
+        want = O.dot(x, y, lb, ub, SCHEDS[sched], chunk, teams, threads)
+        got = float(runtime.dot(xd, yd, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                                threads=threads, mode="ordered").item())
+        assert got == want, (teams, threads, sched)
+
+
+def test_ordered_full_size_bit_exact(cuda):
+    # C2 at full size: 2^30 fp64, the bench geometry and 1024-thread teams;
+    # the oracle regenerates the data itself (reference order, C, all cores)
+    n = 1 << 30
+    x = runtime.synthetic(n, "f64", O.SEED, device=cuda)
+    for teams, threads in ((148, 256), (148, 1024)):
+        want = O.reduce(None, 0, n - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, teams, threads, 0.0)
+        got = _ordered(x, "add", "distribute", 1, teams, threads, 0, n - 1, 0.0)
+        assert got == want, (teams, threads, got, want)
+    del x
+    torch.cuda.empty_cache()
+
+
+def test_ordered_repeated_launches_reuse_workspace(cuda):
+    # per-group ready flags carry a per-launch epoch: back-to-back launches
+    # on one workspace must not see the previous launch's flags
+    n = 3_000_017
+    x = runtime.synthetic(n, "f64", O.SEED, 8, device=cuda)
+    want = O.reduce(None, 0, n - 1, O.F64, O.ADD, O.STATIC, 1, 37, 192, 0.0, k=8)
+    out = torch.zeros(1, dtype=torch.float64, device=cuda)
+    vals = []
+    for _ in range(50):
+        out.zero_()
+        runtime.reduce(x, "add", teams=37, threads=192, mode="ordered", out=out)
+        vals.append(float(out.item()))
+    assert set(vals) == {float(want)}
