@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--unroll", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ordered-steps", type=int, default=50,
+                   help="steps of the ORDERED-mode (reference-order, bit-identical) leg")
     p.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU")
     p.add_argument("--backend", default="nccl",
                    help="torch.distributed backend for N > 1 (gloo: debug the multi-rank "
@@ -291,6 +293,36 @@ def run_ours(args) -> None:
     total_bytes = G * n * ELEM
     gbs = total_bytes * args.steps / (ms_max / 1e3) / 1e9
 
+    # ORDERED mode on the same array and geometry: every OpenMP thread folds
+    # its block in order, partials combined in global thread order — the
+    # reference's own combine order (host.py:567-582), bit-identical to the
+    # CPU reference arm's result (checked against the oracle below)
+    ordered = None
+    if G == 1 and args.ordered_steps > 0:
+        o_out = torch.zeros(1, dtype=torch.float64, device=dev)
+
+        def o_step():
+            o_out.zero_()
+            runtime.reduce(x, "add", sched=args.sched, teams=teams, threads=threads,
+                           mode="ordered", out=o_out)
+
+        for _ in range(3):
+            o_step()
+        torch.cuda.synchronize()
+        got_ordered = float(o_out.item())
+        oa, ob = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        oa.record(stream)
+        for _ in range(args.ordered_steps):
+            o_step()
+        ob.record(stream)
+        torch.cuda.synchronize()
+        o_ms = oa.elapsed_time(ob) / args.ordered_steps
+        ordered = {"value": round(nloc * ELEM / (o_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+                   "ms_per_step": round(o_ms, 5), "steps": args.ordered_steps,
+                   "kernel": "omprt::k_reduce_ordered_rows (row-group cp.async windows + "
+                             "folder warp)",
+                   "result": got_ordered}
+
     # end to end through the C-ABI host-buffer call (pinned host -> HBM each step)
     e2e = None
     if args.e2e_steps > 0:
@@ -329,6 +361,15 @@ def run_ours(args) -> None:
             parity["e2e_rel_err_vs_exact"] = abs(got_e2e - exact) / exact
         if parity["rel_err_vs_exact"] > 1e-6:
             raise SystemExit(f"parity failure: {got} vs exact {exact}")
+        if ordered is not None:
+            # the reference order's exact bits (oracle: the host fallback's
+            # algorithm in C, data regenerated on the host)
+            want = float(O.reduce(None, glb, gub, O.F64, O.ADD,
+                                  {"static": O.STATIC, "distribute": O.DISTRIBUTE}.get(
+                                      args.sched, O.DISTRIBUTE), 1, teams, threads, 0.0))
+            ordered["bit_identical_to_reference_order"] = ordered["result"] == want
+            if not ordered["bit_identical_to_reference_order"]:
+                raise SystemExit(f"ORDERED parity failure: {ordered['result']!r} vs {want!r}")
         r = cpu_reference(1 << 26, 3, 1, teams, threads, min_seconds=10.0)
         cpu = {"value": round(r["gbs"], 3), "unit": "GB/s", "cores": r["cores"], "kind": "port",
                "sample": f"{r['n']} fp64 elements (512 MiB, in host memory) x {r['steps']} "
@@ -372,6 +413,7 @@ def run_ours(args) -> None:
                          "algorithmic_bytes_per_launch": n * ELEM},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "ordered": ordered,
             "gpu_launches": args.steps * (1 if G == 1 else 2),
             "clocks": clocks,
             "parity": parity,

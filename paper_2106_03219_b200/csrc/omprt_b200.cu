@@ -2,6 +2,8 @@
 // Single translation unit: the device runtime, every kernel and the host
 // entry points, so the trap word is one device symbol.
 #include <atomic>
+#include <chrono>
+#include <unistd.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -125,14 +127,19 @@ int sm_count() {
 // ORDERED row-group kernels (ordered.cuh).  Each CTA = nw streaming warps +
 // the folder warp; one CTA per SM (the tile ring takes most of the shared
 // memory), never more CTAs than the warp groups need.  Every launch gets a
-// fresh epoch for the per-group ready flags (so the workspace is reused
-// without re-zeroing).
-std::atomic<uint32_t> g_ord_epoch{0};
+// fresh 64-bit key for the per-group ready flags (so the shared workspace is
+// reused without re-zeroing).
+std::atomic<uint64_t> g_ord_epoch{0};
 
-uint32_t next_epoch() {
-  uint32_t e = ++g_ord_epoch;
-  if (e == 0) e = ++g_ord_epoch;  // 0 is the zeroed workspace's value
-  return e;
+uint64_t next_epoch() {
+  static const uint64_t nonce =
+      (uint64_t)std::chrono::high_resolution_clock::now().time_since_epoch().count() ^
+      ((uint64_t)getpid() << 32);
+  uint64_t z = nonce + 0x9E3779B97F4A7C15ull * (++g_ord_epoch);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z ? z : 1;
 }
 
 inline int ord_grid(int teams, int threads, int nw) {
@@ -536,7 +543,7 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
       const int s256 = OrdSmem<double, 32, 2>::stages_for(nw);
       const int s128 = OrdSmem<double, 16, 2>::stages_for(nw);
       const int grid = ord_grid(teams, threads, nw);
-      const uint32_t ep = next_epoch();
+      const uint64_t ep = next_epoch();
       if (s512 >= 3) {
         const size_t ring = (size_t)nw * OrdSmem<double, 64, 2>::warp_bytes(s512);
         const size_t smem = ring + kFolderSmem;

@@ -65,13 +65,13 @@ OMPRT_D void cp_async_wait(int pending) {
   }
 }
 
-OMPRT_D void st_release_gpu(uint32_t *p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+OMPRT_D void st_release_gpu(uint64_t *p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-OMPRT_D uint32_t ld_acquire_gpu(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+OMPRT_D uint64_t ld_acquire_gpu(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -211,8 +211,8 @@ OMPRT_D void ord_issue(OrdRow<W, 16 / sizeof(T)> &row, const T *const (&src)[NS]
 // group's 32 partials to the folder.
 template <class T, int W, int NS, class Fold>
 OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
-                        const T *const (&src)[NS], int stages, Fold &fold, uint32_t *flags,
-                        uint32_t epoch) {
+                        const T *const (&src)[NS], int stages, Fold &fold, uint64_t *flags,
+                        uint64_t epoch) {
   using L = OrdSmem<T, W, NS>;
   constexpr int V = L::V;
   extern __shared__ __align__(16) unsigned char ord_smem[];
@@ -311,12 +311,6 @@ template <int W> struct OrdDotFold {
   }
 };
 
-OMPRT_D uint32_t ld_relaxed_gpu(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // The folder: one warp (the extra warp of CTA 0) folds the P per-thread
 // partials into *out strictly in global thread order — the fallback's
 // combine order (host.py:567-582) — following the streaming warps as their
@@ -337,7 +331,7 @@ template <class T> struct FoldLoad {
 };
 
 template <class T>
-OMPRT_D void ord_folder_load(const T *tp, int64_t P, const uint32_t *flags, uint32_t epoch,
+OMPRT_D void ord_folder_load(const T *tp, int64_t P, const uint64_t *flags, uint64_t epoch,
                              int64_t b, FoldLoad<T> &L) {
   constexpr int N = FoldLoad<T>::N;
   const uint32_t lane = threadIdx.x & 31u;
@@ -352,7 +346,7 @@ OMPRT_D void ord_folder_load(const T *tp, int64_t P, const uint32_t *flags, uint
 }
 
 template <int OP, class T, class Combine>
-OMPRT_D void ord_folder(const T *tp, int64_t P, const uint32_t *flags, uint32_t epoch, T *out,
+OMPRT_D void ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epoch, T *out,
                         T *ring, Combine &&comb) {
   constexpr int N = FoldLoad<T>::N;
   const uint32_t lane = threadIdx.x & 31u;
@@ -388,7 +382,11 @@ template <int OP, class T> struct RedComb {
   OMPRT_D T operator()(T a, T b) const { return Red<OP, T>::apply(a, b); }
 };
 
-// flags live after the P partials in the (2-slot) thread-partial area
+// flags (one u64 per group) live after the P partials in the (2-slot)
+// thread-partial area.  The workspace is shared with every other kernel, so
+// a flag slot may hold anything when a launch starts: the per-launch key is
+// a splitmix64 image of (process nonce, launch counter) — distinct for every
+// launch of the process and a 2^-64 chance to equal stale data.
 OMPRT_HD size_t ord_flags_offset(int64_t P) { return (size_t)P * 8; }
 
 constexpr int kOrdMaxWarps = 16;  // streaming warps per CTA (+1 folder warp)
@@ -396,10 +394,10 @@ constexpr int kOrdMaxWarps = 16;  // streaming warps per CTA (+1 folder warp)
 template <class T, int OP, int W>
 __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
     k_reduce_ordered_rows(const T *__restrict__ x, LoopArgs la, int teams, int threads,
-                          Workspace ws, T *out, int stages, uint32_t epoch, uint32_t ring_off) {
+                          Workspace ws, T *out, int stages, uint64_t epoch, uint32_t ring_off) {
   const int64_t P = (int64_t)teams * threads;
   T *tp = (T *)ws.thread_partials;
-  uint32_t *flags = (uint32_t *)(ws.thread_partials + ord_flags_offset(P));
+  uint64_t *flags = (uint64_t *)(ws.thread_partials + ord_flags_offset(P));
   if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
     extern __shared__ __align__(16) unsigned char ord_smem[];
     if (blockIdx.x == 0)
@@ -415,10 +413,10 @@ template <int W>
 __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
     k_dot_ordered_rows(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
                        int teams, int threads, Workspace ws, double *out, int stages,
-                       uint32_t epoch, uint32_t ring_off) {
+                       uint64_t epoch, uint32_t ring_off) {
   const int64_t P = (int64_t)teams * threads;
   double *tp = (double *)ws.thread_partials;
-  uint32_t *flags = (uint32_t *)(ws.thread_partials + ord_flags_offset(P));
+  uint64_t *flags = (uint64_t *)(ws.thread_partials + ord_flags_offset(P));
   if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
     extern __shared__ __align__(16) unsigned char ord_smem[];
     if (blockIdx.x == 0)

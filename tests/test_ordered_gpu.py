@@ -124,3 +124,26 @@ def test_ordered_repeated_launches_reuse_workspace(cuda):
         runtime.reduce(x, "add", teams=37, threads=192, mode="ordered", out=out)
         vals.append(float(out.item()))
     assert set(vals) == {float(want)}
+
+
+def test_ordered_ignores_stale_workspace_contents(cuda):
+    # the workspace is shared with every kernel; ready flags must not be
+    # fooled by whatever an earlier launch left there (small integers, old
+    # flags, partials)
+    n = 2_000_003
+    x = runtime.synthetic(n, "f64", O.SEED, 9, device=cuda)
+    want = O.reduce(None, 0, n - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, 64, 320, 0.0, k=9)
+    for pattern in ("ramp32", "ramp64", "ones"):
+        ws = runtime.reduce_workspace(cuda, 64, 320, 2)
+        w32 = ws.view(torch.int32) if ws.numel() % 4 == 0 else None
+        if pattern == "ramp32" and w32 is not None:
+            w32.copy_(torch.arange(w32.numel(), dtype=torch.int32, device=cuda))
+        elif pattern == "ramp64" and ws.numel() % 8 == 0:
+            w64 = ws.view(torch.int64)
+            w64.copy_(torch.arange(w64.numel(), dtype=torch.int64, device=cuda))
+        else:
+            ws.fill_(1)
+        ws.view(torch.uint32)[:64].zero_()  # the ticket word starts at 0
+        got = _ordered(x, "add", "distribute", 1, 64, 320, 0, n - 1, 0.0)
+        assert got == want, pattern
+    runtime.reduce_workspace(cuda, 64, 320, 2).zero_()
