@@ -37,18 +37,19 @@ namespace omprt {
 
 constexpr int kOrdSmemBudget = 216 * 1024;  // dynamic smem of a CTA's streaming warps
 
+// No "memory" clobber on the copies themselves (the commit/wait carry it):
+// that lets the compiler batch the window-table loads ahead of the copies.
 OMPRT_D void cp_async_16(void *smem_dst, const void *gsrc) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(d), "l"(gsrc)
-               : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc));
 }
 
 template <int BYTES> OMPRT_D void cp_async_small(void *smem_dst, const void *gsrc) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
   if (BYTES == 8)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc));
   else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc));
 }
 
 OMPRT_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
