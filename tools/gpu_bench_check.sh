@@ -1,0 +1,4 @@
+set -x
+mkdir -p gpurun_out
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 100 --warmup 3 --e2e-steps 1 --backend gloo > gpurun_out/tr2_gloo.log 2>&1
