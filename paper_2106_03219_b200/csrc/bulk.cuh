@@ -307,8 +307,10 @@ __global__ void __launch_bounds__(kMaxThreads)
 
 // Chunked-schedule axpy + max/min over the TMA ring: x and y arrive by bulk
 // copy, the new y leaves by coalesced 16-byte stores.
-template <int STAGES, int STAGE_BYTES, int U>
-__global__ void __launch_bounds__(kMaxThreads)
+// MAXT: launch bound (256 for the default 148x256 grid: no 64-register cap,
+// no spills; kMaxThreads for bigger teams).
+template <int STAGES, int STAGE_BYTES, int U, int MAXT = kMaxThreads>
+__global__ void __launch_bounds__(MAXT)
     k_axpy_minmax_bulk(float a, const float *__restrict__ x, float *__restrict__ y, LoopArgs la,
                        Workspace ws, float *out_max, float *out_min) {
   extern __shared__ __align__(128) unsigned char stages[];

@@ -516,7 +516,8 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
   if (mode == OMPRT_MODE_ORDERED) {
     k_axpy_minmax_ordered<<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
   } else if (bulk_ok) {
-    auto kern = k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
+    auto kern = threads <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
+                               : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
     if ((rc = set_smem(kern, smem))) return rc;
     kern<<<teams, threads, smem, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
