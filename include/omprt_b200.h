@@ -133,8 +133,9 @@ int omprt_set_unroll(int unroll);
 /* Tuning knob (not part of the reference interface): kernel variant used by
  * the fp64 sum in SPMD mode — 0 default; 1-5 LDG load-policy / unroll
  * variants; 10-16 TMA bulk-copy (cp.async.bulk + mbarrier) stage rings;
- * 20 = ORDERED mode through the literal per-thread walk instead of the staged
- * (cp.async shared-memory window) kernels. */
+ * 20 = ORDERED mode through the literal per-thread walk instead of the
+ * row-group kernels (cp.async shared-memory row windows + folder warp);
+ * 21-27 = row-group kernels with a forced window size x warps per SM. */
 int omprt_set_variant(int variant);
 
 /* Number of streaming multiprocessors of the current device (148 on B200). */
@@ -174,10 +175,12 @@ int omprt_bounds_dump(int64_t lb, int64_t ub, int sched, int64_t chunk, int team
 /* ========================================================================= */
 
 /* Bytes of device workspace the reductions need (team partials, per-thread
- * partials for ORDERED, the last-team-finishes ticket).  The workspace must be
- * zeroed once before first use; the ticket self-resets (atomic inc wraps,
- * devicert.step_inc devicert.py:105-107), so it can be reused across launches
- * on one stream. */
+ * partials for ORDERED, the last-team-finishes ticket, ORDERED's per-group
+ * ready flags).  The workspace must be zeroed once before first use; the
+ * ticket self-resets (atomic inc wraps, devicert.step_inc
+ * devicert.py:105-107) and the ready flags carry a fresh 64-bit key per
+ * launch, so it can be reused across launches (of any kernel) on one
+ * stream. */
 size_t omprt_reduce_workspace_bytes(int teams, int threads, int mode);
 
 /* out = out OP reduce_{i in [lb,ub]} x[i], x indexed by the iteration number
