@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
   __shared__ double scratch[32];
-  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  const TeamSet s = team_set_cta(la);
   DotBody body(x, y);
   BulkPlan<STAGE_BYTES> plan;
   const void *const ptrs[2] = {x, y};
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(MAXT)
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
   __shared__ float scratch[32];
-  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  const TeamSet s = team_set_cta(la);
   AxpyBody body(a, x, y);
   BulkPlan<STAGE_BYTES> plan;
   const void *const ptrs[2] = {x, y};
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
   __shared__ T scratch[32];
-  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  const TeamSet s = team_set_cta(la);
   ReduceBody<T, OP> body(x);
   BulkPlan<STAGE_BYTES> plan;
   const void *const ptrs[1] = {x};

@@ -25,8 +25,15 @@ struct Workspace {
   unsigned char *thread_partials;
 };
 
+// Team-partial slots: at least kMinPartialSlots so an SPMD launch may split
+// each of a few teams over several CTAs (LoopArgs::split, team_set_cta).
+constexpr int kMinPartialSlots = 256;
+__host__ __device__ inline int partial_slots(int teams) {
+  return teams < kMinPartialSlots ? kMinPartialSlots : teams;
+}
+
 __host__ inline size_t ws_bytes(int teams, int threads, int mode, int slots) {
-  size_t b = 256 + (size_t)teams * 8 * slots;
+  size_t b = 256 + (size_t)partial_slots(teams) * 8 * slots;
   b = (b + 255) & ~(size_t)255;
   if (mode == OMPRT_MODE_ORDERED) b += (size_t)teams * threads * 8 * slots;
   return b;
@@ -37,7 +44,7 @@ __host__ inline Workspace ws_carve(void *base, int teams, int slots) {
   unsigned char *p = (unsigned char *)base;
   w.ticket = (uint32_t *)p;
   w.team_partials = p + 256;
-  size_t off = 256 + (size_t)teams * 8 * slots;
+  size_t off = 256 + (size_t)partial_slots(teams) * 8 * slots;
   off = (off + 255) & ~(size_t)255;
   w.thread_partials = p + off;
   return w;
@@ -233,13 +240,61 @@ struct AxpyBody {
 struct LoopArgs {
   int64_t lb, ub, chunk;
   int sched;
+  int split;  // SPMD: CTAs per OpenMP team (<= 1: one CTA per team)
 };
+
+// The iteration set of this CTA: its team's set (team_set, the schedule's
+// contract) — or, when a launch splits each team over `split` CTAs (few
+// teams: the rest of the SMs would idle), sub-CTA k's share of it: a
+// contiguous set cut into split pieces on 64-element boundaries, a comb's
+// teeth dealt round robin.  Which CTA of the team folds an iteration is as
+// unobservable as which lane does (SPMD re-association; integers exact), and
+// the team partials are still combined in (team, piece) order.
+OMPRT_D TeamSet team_set_cta(const LoopArgs &la) {
+  const int64_t cl = la.split > 1 ? la.split : 1;
+  const int64_t teams = gridDim.x / cl, team = blockIdx.x / cl, sub = blockIdx.x % cl;
+  TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, team, teams, blockDim.x);
+  if (cl == 1 || s.nseg <= 0) return s;
+  if (s.seg_stride == 0 || s.nseg <= 1) {
+    int64_t len = s.ub - s.first + 1;
+    if (len > s.seg_len) len = s.seg_len;
+    const int64_t end = s.first + len;
+    const int64_t piece = (len + cl - 1) / cl;
+    // cut points on absolute 64-element boundaries (16-byte aligned pieces)
+    auto cut = [&](int64_t k) {
+      if (k <= 0) return s.first;
+      if (k >= cl) return end;
+      int64_t c = (s.first + k * piece + 63) & ~(int64_t)63;
+      return c < end ? c : end;
+    };
+    const int64_t lo = cut(sub), hi = cut(sub + 1);
+    if (hi <= lo) {
+      s.nseg = 0;
+      s.seg_len = 0;
+      return s;
+    }
+    s.first = lo;
+    s.seg_len = hi - lo;
+    s.nseg = 1;
+    s.seg_stride = 0;
+    s.ub = hi - 1;
+    return s;
+  }
+  if (sub >= s.nseg) {
+    s.nseg = 0;
+    return s;
+  }
+  s.first += sub * s.seg_stride;
+  s.nseg = (s.nseg - sub + cl - 1) / cl;
+  s.seg_stride *= cl;
+  return s;
+}
 
 template <class T, int OP, int U, int LP = kLoadDefault, int VB = 16>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
   __shared__ T scratch[32];
-  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  const TeamSet s = team_set_cta(la);
   ReduceBody<T, OP, LP, VB> body(x);
   run_team<U>(body, s, threadIdx.x, blockDim.x);
   const T team_val = block_reduce<OP, T>(body.total(), scratch, blockDim.x);
@@ -317,7 +372,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     k_dot(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la, Workspace ws,
           double *out) {
   __shared__ double scratch[32];
-  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  const TeamSet s = team_set_cta(la);
   DotBody body(x, y);
   run_team<U>(body, s, threadIdx.x, blockDim.x);
   const double team_val = block_reduce<OMPRT_OP_ADD, double>(body.total(), scratch, blockDim.x);
@@ -351,7 +406,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     k_axpy_minmax(float a, const float *__restrict__ x, float *__restrict__ y, LoopArgs la,
                   Workspace ws, float *out_max, float *out_min) {
   __shared__ float scratch[32];
-  const TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x, blockDim.x);
+  const TeamSet s = team_set_cta(la);
   AxpyBody body(a, x, y);
   run_team<U>(body, s, threadIdx.x, blockDim.x);
   const float tmax = block_reduce<OMPRT_OP_MAX, float>(body.max_total(), scratch, blockDim.x);

@@ -83,7 +83,7 @@ int launch_bulk(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T
   const size_t smem = BulkSmem<STAGES, SB>::bytes;
   int rc = set_smem(kern, smem);
   if (rc) return rc;
-  kern<<<teams, threads, smem, st>>>(xp, la, w, op);
+  kern<<<teams * (la.split > 1 ? la.split : 1), threads, smem, st>>>(xp, la, w, op);
   return check_launch("omprt_reduce(bulk)");
 }
 
@@ -122,6 +122,19 @@ int sm_count() {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return 0;
   return sms;
+}
+
+// SPMD launches with few teams split every team over `split` CTAs
+// (team_set_cta) so the whole GPU streams: split = SMs / teams (<= 16) when
+// teams <= SMs / 2.  Variant kNoSplit keeps one CTA per team.
+constexpr int kNoSplit = 30;
+
+int spmd_split(int teams) {
+  if (g_variant == kNoSplit) return 1;
+  const int sms = sm_count();
+  if (sms <= 0 || teams * 2 > sms) return 1;
+  int cl = sms / teams;
+  return cl > 16 ? 16 : cl;
 }
 
 // ORDERED row-group kernels (ordered.cuh).  Each CTA = nw streaming warps +
@@ -224,15 +237,19 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
     } else {
       k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
     }
-  } else if (bulk_ok) {
-    // default SPMD path: TMA bulk-copy stage ring
-    return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, threads, w, op, st);
-  } else if (g_unroll >= 8) {
-    k_reduce<T, OP, 8><<<teams, threads, 0, st>>>(xp, la, w, op);
-  } else if (g_unroll <= 2) {
-    k_reduce<T, OP, 2><<<teams, threads, 0, st>>>(xp, la, w, op);
   } else {
-    k_reduce<T, OP, 4><<<teams, threads, 0, st>>>(xp, la, w, op);
+    la.split = spmd_split(teams);
+    const int grid = teams * la.split;
+    if (bulk_ok) {
+      // default SPMD path: TMA bulk-copy stage ring
+      return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, threads, w, op, st);
+    } else if (g_unroll >= 8) {
+      k_reduce<T, OP, 8><<<grid, threads, 0, st>>>(xp, la, w, op);
+    } else if (g_unroll <= 2) {
+      k_reduce<T, OP, 2><<<grid, threads, 0, st>>>(xp, la, w, op);
+    } else {
+      k_reduce<T, OP, 4><<<grid, threads, 0, st>>>(xp, la, w, op);
+    }
   }
   return check_launch("omprt_reduce");
 }
@@ -516,13 +533,16 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
   if (mode == OMPRT_MODE_ORDERED) {
     k_axpy_minmax_ordered<<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
   } else if (bulk_ok) {
+    la.split = spmd_split(teams);
     auto kern = threads <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
                                : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
     if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams, threads, smem, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+    kern<<<teams * la.split, threads, smem, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
   } else {
-    k_axpy_minmax<4><<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+    la.split = spmd_split(teams);
+    k_axpy_minmax<4><<<teams * la.split, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max,
+                                                                   d_min);
   }
   return check_launch("omprt_axpy_minmax");
 }
@@ -568,14 +588,18 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
       k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
     }
   } else if (bulk_ok) {
+    la.split = spmd_split(teams);
     auto kern = k_dot_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
     if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams, threads, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
-  } else if (g_unroll >= 8)
-    k_dot<8><<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
-  else
-    k_dot<4><<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+    kern<<<teams * la.split, threads, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
+  } else {
+    la.split = spmd_split(teams);
+    if (g_unroll >= 8)
+      k_dot<8><<<teams * la.split, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+    else
+      k_dot<4><<<teams * la.split, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+  }
   return check_launch("omprt_dot");
 }
 

@@ -240,3 +240,31 @@ def test_comb_bulk_plans(cuda, dtype):
             assert abs(float(got) - exact) <= 1e-9 * exact
         else:
             assert int(got) == int(want), (teams, threads, chunk, lb, ub)
+
+
+@pytest.mark.parametrize("sched", list(SCHEDS))
+def test_team_split_matches_one_cta_per_team(cuda, sched):
+    # few teams: each team is split over several CTAs (team_set_cta); integer
+    # results must equal the one-CTA-per-team launch (variant 30) and the
+    # oracle bit for bit, for contiguous and comb team sets
+    n = 1_500_007
+    x = O.fill(n, O.I64, O.SEED, 12)
+    xd = torch.from_numpy(x).to(cuda)
+    try:
+        for teams, threads, lb, ub, chunk in ((1, 128, 0, n - 1, 1), (1, 128, 3, n - 5, 64),
+                                              (2, 256, 1, n - 1, 4096), (5, 96, 0, 700_000, 7),
+                                              (9, 1024, 0, n - 1, 300), (3, 64, 10, 5000, 1)):
+            want = O.reduce(x, lb, ub, O.I64, O.ADD, SCHEDS[sched], chunk, teams, threads, 0)
+            got = run_reduce(cuda, x, O.I64, "add", sched, chunk, teams, threads, lb, ub)
+            runtime.set_variant(30)
+            one = run_reduce(cuda, x, O.I64, "add", sched, chunk, teams, threads, lb, ub)
+            runtime.set_variant(0)
+            assert int(got) == int(want) == int(one), (teams, threads, lb, ub, chunk)
+            # fp64 through the split path stays within the SPMD tolerance
+            xf = runtime.synthetic(n, "f64", O.SEED, 12, device=cuda)
+            gf = float(runtime.reduce(xf, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                                      threads=threads).item())
+            ex = O.exact_sum_gen(lb, ub, O.F64, k=12)
+            assert abs(gf - ex) <= 1e-6 * ex
+    finally:
+        runtime.set_variant(0)

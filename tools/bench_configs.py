@@ -58,7 +58,8 @@ def main():
     x = runtime.synthetic(n, "i64", SEED, device=dev)
     out = torch.zeros(1, dtype=torch.int64, device=dev)
     ms = timeit(lambda: runtime.reduce(x, teams=1, threads=128, out=out), a.reps)
-    line("C1 int64 sum static 1x128 N=2^20", ms, n * 8, note="one team: latency-bound by design")
+    line("C1 int64 sum static 1x128 N=2^20", ms, n * 8,
+         note="one OpenMP team split over 16 CTAs (team_set_cta); L2-resident after the first pass")
     ms = timeit(lambda: runtime.reduce(x, out=out), a.reps)
     line("C1 int64 sum N=2^20, default grid", ms, n * 8, teams=sms, threads=256,
          note="L2-resident after the first pass")
