@@ -1,6 +1,7 @@
 # ncu evidence for the bench's dominant kernel (one GPU, never multi-rank)
 set -x
 mkdir -p gpurun_out
-B="python bench.py --e2e-steps 0 --no-cpu-baseline"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv $B --steps 20 --warmup 2 > gpurun_out/ncu_launch.log 2>&1
+B="python bench.py --e2e-steps 0 --no-cpu-baseline --ordered-steps 5"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $B --steps 20 --warmup 3 > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reduce_bulk -s 3 -c 1 -o gpurun_out/prof_bench $B --steps 5 --warmup 1 > gpurun_out/ncu_full.log 2>&1
+gzip -f gpurun_out/prof_bench.ncu-rep
