@@ -18,6 +18,18 @@ for sched in ("static", "static_chunked", "distribute", "distribute_chunked"):
         runtime.reduce(xi, "max", lb=3, ub=99_000, sched=sched, chunk=7, teams=5, threads=96, mode=mode)
         runtime.axpy_minmax(0.5, xf, yf, sched=sched, chunk=64, teams=8, threads=256, mode=mode)
         runtime.dot(x, x, sched=sched, chunk=64, teams=8, threads=256, mode=mode)
+# ORDERED row-group kernels: windows touching lb/ub (element-checked copies),
+# OpenMP thread counts that are not multiples of 32, the folder's partial batch
+runtime.reduce(x, lb=1, ub=100_001, sched="static", teams=7, threads=33, mode="ordered")
+runtime.reduce(xf, lb=3, ub=100_000, sched="distribute", teams=3, threads=100, mode="ordered")
+runtime.dot(x, x, lb=5, ub=99_999, sched="static_chunked", chunk=40, teams=9, threads=64,
+            mode="ordered")
+runtime.set_variant(20)
+runtime.reduce(x, sched="distribute", teams=8, threads=256, mode="ordered")
+runtime.set_variant(0)
+# few-team SPMD launches split over CTAs (team_set_cta)
+runtime.reduce(xi, sched="static", teams=1, threads=128)
+runtime.reduce(x, sched="static_chunked", chunk=5, teams=3, threads=64)
 runtime.set_unroll(8)
 runtime.reduce(x, teams=8, threads=256)
 runtime.set_unroll(4)
