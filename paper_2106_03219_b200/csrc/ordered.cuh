@@ -161,30 +161,36 @@ OMPRT_D void ord_issue(OrdRow<W, 16 / sizeof(T)> &row, const T *const (&src)[NS]
                        int64_t ub, longlong2 *table, T *tiles, int st, uint32_t lane) {
   using L = OrdSmem<T, W, NS>;
   constexpr int V = L::V, U = L::U;
-  static_assert((U & (U - 1)) == 0, "units per window must be a power of two");
+  static_assert((U & (U - 1)) == 0 && U <= 32, "units per window: a power of two <= 32");
+  constexpr int RPI = 32 / U;  // rows per copy instruction; j = lane % U is lane-constant
   const bool live = row.live();
   const bool inside = !live || (row.a >= lb && row.a + W - 1 <= ub);
-  table[lane] = make_longlong2(row.a, live ? (long long)row.e() : -1ll);
   const bool fast = __all_sync(0xffffffffu, inside);
-  __syncwarp();  // table writes visible to the warp
   T *tile0 = tiles + (size_t)st * NS * (L::kTile / sizeof(T));
+  const int j = (int)(lane % U), rsub = (int)(lane / U);
   if (fast) {
-#pragma unroll 8
+    // table: the window's byte address in stream 0 and its unit count
+    table[lane] = make_longlong2((long long)(uintptr_t)(src[0] + row.a),
+                                 live ? (long long)(row.e() / V + 1) : 0ll);
+    __syncwarp();
+    T *dlane = tile0 + rsub * L::RS + j * V;
+#pragma unroll
     for (int i = 0; i < U; ++i) {
-      const int f = i * 32 + (int)lane;
-      const int r = f / U, j = f % U;
-      const longlong2 en = table[r];
-      if (j * V <= (int)en.y) {
+      const longlong2 en = table[i * RPI + rsub];
+      if (j < (int)en.y) {
+        const char *g = (const char *)(uintptr_t)en.x + j * 16;
 #pragma unroll
         for (int s = 0; s < NS; ++s)
-          cp_async_16(tile0 + (size_t)s * (L::kTile / sizeof(T)) + r * L::RS + j * V,
-                      src[s] + en.x + j * V);
+          cp_async_16(dlane + (size_t)s * (L::kTile / sizeof(T)) + i * RPI * L::RS,
+                      g + ((const char *)src[s] - (const char *)src[0]));
       }
     }
   } else {
+    // windows touching lb or ub: element-checked copies
+    table[lane] = make_longlong2(row.a, live ? (long long)row.e() : -1ll);
+    __syncwarp();
     for (int i = 0; i < U; ++i) {
-      const int f = i * 32 + (int)lane;
-      const int r = f / U, j = f % U;
+      const int r = i * RPI + rsub;
       const longlong2 en = table[r];
       if (j * V <= (int)en.y) {
         const int64_t e0 = en.x + (int64_t)j * V;
@@ -231,13 +237,17 @@ OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
     fd = ld;
     for (int s = 0; s + 1 < stages; ++s)
       ord_issue<T, W, NS>(ld, src, la.lb, la.ub, table, tiles, s, lane);
-    for (int t = 0;; ++t) {
+    // ring positions kept incrementally (stages is a runtime value: no modulo)
+    int st_fold = 0, st_issue = stages - 1;
+    for (;;) {
       if (!__any_sync(0xffffffffu, fd.live())) break;
-      ord_issue<T, W, NS>(ld, src, la.lb, la.ub, table, tiles, (t + stages - 1) % stages, lane);
+      ord_issue<T, W, NS>(ld, src, la.lb, la.ub, table, tiles, st_issue, lane);
+      st_issue = (st_issue + 1 == stages) ? 0 : st_issue + 1;
       cp_async_wait(stages - 1);
       __syncwarp();
+      const int st = st_fold;
+      st_fold = (st_fold + 1 == stages) ? 0 : st_fold + 1;
       if (fd.live()) {
-        const int st = t % stages;
         const T *rows[NS];
 #pragma unroll
         for (int s = 0; s < NS; ++s)
