@@ -2,14 +2,20 @@
 headline is bench.py).  Back-to-back CUDA-event timing after warm-up; GB/s of
 algorithmic bytes; fraction of the measured copy peak and of nominal 8 TB/s.
 
-    python tools/bench_configs.py [--reps 200] > profiles/<round>_configs.jsonl
+    python tools/bench_configs.py [--reps 200] [--cpu] > profiles/<round>_configs.jsonl
+
+--cpu times the CPU reference (the oracle's C restatement of the host
+fallback's algorithm, all host cores, bounded in-memory samples) beside every
+config: "cpu_reference" and "gpu_over_cpu" in each line.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
+import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -38,18 +44,50 @@ def timeit(fn, reps, warm=10):
     return a.elapsed_time(b) / reps
 
 
-def line(config, ms, nbytes, **kw):
+CPU = {"on": False}
+
+
+def cpu_ref(fn, nbytes, min_s=2.0):
+    """The reference's CPU algorithm restated in C (oracle/, kind "port") on
+    a bounded in-memory sample, all host cores: GB/s of the same
+    algorithmic bytes.  Only timed with --cpu (test infrastructure as a
+    baseline leg, never the measured product)."""
+    if not CPU["on"]:
+        return None
+    fn()
+    t0 = time.perf_counter()
+    k = 0
+    while k < 2 or time.perf_counter() - t0 < min_s:
+        fn()
+        k += 1
+    dt = (time.perf_counter() - t0) / k
+    return {"gbs": round(nbytes / dt / 1e9, 2), "ms": round(dt * 1e3, 3), "cores": CPU["cores"],
+            "kind": "port", "sample_bytes": nbytes}
+
+
+def line(config, ms, nbytes, cpu=None, **kw):
     gbs = nbytes / ms / 1e6
     rec = {"config": config, "ms": round(ms, 5), "gbs": round(gbs, 1),
            "frac_measured_peak": round(gbs / PEAK, 4), "frac_nominal_8tbs": round(gbs / 8000, 4)}
     rec.update(kw)
+    if cpu is not None:
+        rec["cpu_reference"] = cpu
+        rec["gpu_over_cpu"] = round(gbs / cpu["gbs"], 1)
     print(json.dumps(rec), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--cpu", action="store_true",
+                    help="time the CPU reference (oracle port, all host cores) beside each config")
     a = ap.parse_args()
+    if a.cpu:
+        from oracle import oracle as O
+
+        CPU["on"] = True
+        CPU["cores"] = len(os.sched_getaffinity(0))
+        O.set_threads(CPU["cores"])
     dev = torch.device("cuda", 0)
     sms = runtime.num_sms()
 
@@ -58,7 +96,11 @@ def main():
     x = runtime.synthetic(n, "i64", SEED, device=dev)
     out = torch.zeros(1, dtype=torch.int64, device=dev)
     ms = timeit(lambda: runtime.reduce(x, teams=1, threads=128, out=out), a.reps)
-    line("C1 int64 sum static 1x128 N=2^20", ms, n * 8,
+    c1 = None
+    if CPU["on"]:
+        xh = O.fill(n, O.I64, SEED)
+        c1 = cpu_ref(lambda: O.reduce(xh, 0, n - 1, O.I64, O.ADD, O.STATIC, 1, 1, 128), n * 8)
+    line("C1 int64 sum static 1x128 N=2^20", ms, n * 8, cpu=c1,
          note="one OpenMP team split over 16 CTAs (team_set_cta); L2-resident after the first pass")
     ms = timeit(lambda: runtime.reduce(x, out=out), a.reps)
     line("C1 int64 sum N=2^20, default grid", ms, n * 8, teams=sms, threads=256,
@@ -70,7 +112,13 @@ def main():
     x = runtime.synthetic(n, "f64", SEED, device=dev)
     outf = torch.zeros(1, dtype=torch.float64, device=dev)
     ms = timeit(lambda: runtime.reduce(x, sched="distribute", out=outf), a.reps)
-    line("C2 fp64 sum distribute SPMD N=2^30", ms, n * 8, teams=sms, threads=256)
+    c2 = None
+    if CPU["on"]:
+        ns = 1 << 26
+        xh = O.fill(ns, O.F64, SEED)
+        c2 = cpu_ref(lambda: O.reduce(xh, 0, ns - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, sms, 256),
+                     ns * 8)
+    line("C2 fp64 sum distribute SPMD N=2^30", ms, n * 8, cpu=c2, teams=sms, threads=256)
     for sched in ("static", "distribute_chunked", "static_chunked"):
         ms = timeit(lambda: runtime.reduce(x, sched=sched, chunk=64, out=outf), a.reps // 4)
         line(f"C2 fp64 sum {sched} chunk=64 N=2^30", ms, n * 8, teams=sms, threads=256)
@@ -87,7 +135,12 @@ def main():
     # C5 shard: fp64 dot over 2^30 (16 B / iteration)
     y = runtime.synthetic(n, "f64", SEED, 1, device=dev)
     ms = timeit(lambda: runtime.dot(x, y, out=outf), a.reps // 2)
-    line("C5 fp64 dot N=2^30 per GPU shard", ms, n * 16, teams=sms, threads=256)
+    c5 = None
+    if CPU["on"]:
+        ns = 1 << 25
+        xh, yh = O.fill(ns, O.F64, SEED, 0), O.fill(ns, O.F64, SEED, 1)
+        c5 = cpu_ref(lambda: O.dot(xh, yh, 0, ns - 1, O.DISTRIBUTE, 1, sms, 256), ns * 16)
+    line("C5 fp64 dot N=2^30 per GPU shard", ms, n * 16, cpu=c5, teams=sms, threads=256)
     del x, y, xi
     torch.cuda.empty_cache()
 
@@ -101,7 +154,15 @@ def main():
         for chunk in (1, 64, 4096):
             ms = timeit(lambda: runtime.axpy_minmax(1e-7, xs, ys, sched=sched, chunk=chunk,
                                                     out_max=mx, out_min=mn), a.reps // 2)
-            line(f"C3 axpy+max/min {sched} chunk={chunk} N=2^28", ms, n * 12)
+            c3 = None
+            if CPU["on"]:
+                ns = 1 << 26
+                xh, yh = O.fill(ns, O.F32, SEED, 0), O.fill(ns, O.F32, SEED, 1)
+                code = {"distribute_chunked": O.DISTRIBUTE_CHUNKED,
+                        "static_chunked": O.STATIC_CHUNKED}[sched]
+                c3 = cpu_ref(lambda: O.axpy_minmax(1e-7, xh, yh, 0, ns - 1, code, chunk, sms, 256,
+                                                   float("-inf"), float("inf")), ns * 12)
+            line(f"C3 axpy+max/min {sched} chunk={chunk} N=2^28", ms, n * 12, cpu=c3)
     del xs, ys
     torch.cuda.empty_cache()
 
@@ -113,8 +174,13 @@ def main():
         for ordered in (False, True):
             ms = timeit(lambda: runtime.generic_reduce(x, teams=1024, par_threads=256,
                                                        ordered=ordered, out=o), a.reps // 2)
+            c4 = None
+            if CPU["on"] and ordered:
+                dt = O.I64 if dtype == "i64" else O.F64
+                xh = O.fill(n, dt, SEED, 4)
+                c4 = cpu_ref(lambda: O.generic_reduce(xh, 0, n - 1, dt, O.ADD, 1024, 256), n * 8)
             line(f"C4 generic {dtype} 1024 teams x (32+256) {'ordered' if ordered else 'spmd'}"
-                 " N=2^26", ms, n * 8)
+                 " N=2^26", ms, n * 8, cpu=c4)
         del x
     torch.cuda.empty_cache()
 
