@@ -65,7 +65,10 @@ enum omprt_sched {
  *  ORDERED  every device thread runs exactly its own schedule chunks in
  *           iteration order and the per-thread partials are combined in
  *           global thread order — the host fallback's order (host.py:567-582),
- *           so fp results are bit-identical to the CPU reference order */
+ *           so fp results are bit-identical to the CPU reference order.
+ *           Integer reductions give the same bits in either order (add wraps
+ *           mod 2^n, max/min are exact), so ORDERED integer launches run the
+ *           SPMD kernels. */
 enum omprt_mode { OMPRT_MODE_SPMD = 0, OMPRT_MODE_ORDERED = 1 };
 
 /* ---- status and trap kinds (TrapKind / TRAP_CODES, vgpu.py:28-43) */

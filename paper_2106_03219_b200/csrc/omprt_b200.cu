@@ -225,16 +225,24 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
       return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
   }
   const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
+  // Integer add (mod 2^n), max and min are associative and commutative: the
+  // reference order's result IS the re-associated one, bit for bit, so
+  // ORDERED integer reductions take the SPMD kernels (variant kOrderedLiteral
+  // still forces the literal walk, for the tests).
+  if (mode == OMPRT_MODE_ORDERED && std::is_integral<T>::value && g_variant != kOrderedLiteral)
+    mode = OMPRT_MODE_SPMD;
   if (mode == OMPRT_MODE_ORDERED) {
-    // staged per-thread windows (ordered.cuh); the literal walk for small
-    // chunks, partial warps, or variant kOrderedLiteral
+    // row-group kernels (ordered.cuh); the literal walk for small chunks,
+    // pointers not 16-byte aligned, or variant kOrderedLiteral
     if constexpr (std::is_same<T, double>::value && OP == OMPRT_OP_ADD) {
       if (g_variant > kOrderedLiteral && g_variant < 30)
         return launch_ordered_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
     }
-    if (g_variant != kOrderedLiteral && ord_rows_ok(la, x)) {
-      return launch_ordered_default<T, OP>(xp, la, teams, threads, w, op, st);
-    } else {
+    if constexpr (std::is_floating_point<T>::value) {
+      if (g_variant != kOrderedLiteral && ord_rows_ok(la, x))
+        return launch_ordered_default<T, OP>(xp, la, teams, threads, w, op, st);
+    }
+    {
       k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
     }
   } else {

@@ -1,4 +1,5 @@
-"""ORDERED mode through the row-group kernels (csrc/ordered.cuh): every
+"""ORDERED mode (fp: the row-group kernels of csrc/ordered.cuh; integers: the
+SPMD kernels, whose wrapping/exact combine gives the same bits): every
 OpenMP thread's in-order fold and the global-thread-order combine must be
 bit-identical to the reference order (host.py:567-582) restated in
 oracle/omprt_oracle.c — for fp too — on every geometry: threads not a
