@@ -385,6 +385,9 @@ int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, in
                      int64_t pad, ArenaCfg cfg, Workspace w, void *out, int64_t *offs,
                      cudaStream_t st) {
   auto kern = k_generic<T, OP, 4>;
+  // integer folds give the same bits in any order (see launch_reduce_t):
+  // the ordered worker loop is only needed for fp
+  if (std::is_integral<T>::value && g_variant != kOrderedLiteral) ordered = 0;
   // Physical backing of the team arena: the region's known allocation
   // footprint (pad, then parts[P+1]) capped at the semantic capacity.  The
   // overflow check still uses cfg.capacity (64 KiB, the reference's
