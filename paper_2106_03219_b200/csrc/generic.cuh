@@ -298,9 +298,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         // for_static_init over the team block, literal sequential chunk
         int64_t mlb, mub;
         static_bounds(tlb, tub, wt, P, mlb, mub);
-        T part = Red<OP, T>::identity();
-        for (int64_t i = mlb; i <= mub; ++i) part = Red<OP, T>::apply(part, x[i]);
-        parts[wt] = part;
+        parts[wt] = fold_row_in_order<OP, T>(x, mlb, mub, Red<OP, T>::identity());
       } else {
         // 256-bit streaming loads: the worker warps share the SM with other
         // teams, so each lane keeps U x 32 bytes in flight

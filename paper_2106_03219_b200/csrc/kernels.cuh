@@ -348,14 +348,50 @@ OMPRT_D T fold_in_order_team(T acc, const T *p, int64_t n, T *buf, int cap) {
   return acc;
 }
 
+// One OpenMP thread's literal in-order fold of x[lo..hi] (the fallback's
+// per-thread loop, host.py:567-582), fed by 32-byte loads (LDG.E.256) with
+// 256-byte L2 promotion: every DRAM access brings 256 B of the thread's own
+// row, which its next seven loads then find in L2 — the rows of a warp are
+// far apart, so without the promotion DRAM would see 32-byte pieces.
+template <int OP, class T>
+OMPRT_D T fold_row_in_order(const T *__restrict__ x, int64_t lo, int64_t hi, T part) {
+  constexpr int V = 32 / (int)sizeof(T);
+  int64_t i = lo;
+  for (; i <= hi && (((uintptr_t)(x + i)) & 31u) != 0; ++i) part = Red<OP, T>::apply(part, x[i]);
+  for (; i + 2 * V - 1 <= hi; i += 2 * V) {
+    const U8x32 a = ld_v8<kLoadNcL2_256B>(x + i);
+    const U8x32 b = ld_v8<kLoadNcL2_256B>(x + i + V);
+    T va[V], vb[V];
+    memcpy(va, &a, 32);
+    memcpy(vb, &b, 32);
+#pragma unroll
+    for (int k = 0; k < V; ++k) part = Red<OP, T>::apply(part, va[k]);
+#pragma unroll
+    for (int k = 0; k < V; ++k) part = Red<OP, T>::apply(part, vb[k]);
+  }
+  for (; i <= hi; ++i) part = Red<OP, T>::apply(part, x[i]);
+  return part;
+}
+
 constexpr int kFoldBuf = 2048;  // elements of the static fold buffer
 
 template <class T, int OP>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce_ordered(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
   T part = Red<OP, T>::identity();
-  run_thread_chunks(la.sched, la.lb, la.ub, la.chunk,
-                    [&](int64_t i) { part = Red<OP, T>::apply(part, x[i]); });
+  {
+    const Bounds bd = schedule_init(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x,
+                                    threadIdx.x, blockDim.x);
+    if (la.sched != OMPRT_SCHED_STATIC_CHUNKED && la.sched != OMPRT_SCHED_DISTRIBUTE_CHUNKED) {
+      part = fold_row_in_order<OP, T>(x, bd.lower, bd.upper, part);
+    } else {
+      for (int64_t lo = bd.lower; lo <= bd.limit; lo += bd.stride) {
+        int64_t hi = lo + la.chunk - 1;
+        if (hi > bd.limit) hi = bd.limit;
+        part = fold_row_in_order<OP, T>(x, lo, hi, part);
+      }
+    }
+  }
   __shared__ T buf[kFoldBuf];
   T *tp = (T *)ws.thread_partials;
   tp[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = part;
