@@ -588,12 +588,14 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
         if ((rc = set_smem(k_dot_ordered_rows<32>, smem))) return rc;
         k_dot_ordered_rows<32><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
             d_x, d_y, la, teams, threads, w, d_out, s256, ep, (uint32_t)ring);
-      } else {
+      } else if (s128 >= 2) {
         const size_t ring = (size_t)nw * OrdSmem<double, 16, 2>::warp_bytes(s128);
         const size_t smem = ring + kFolderSmem;
         if ((rc = set_smem(k_dot_ordered_rows<16>, smem))) return rc;
         k_dot_ordered_rows<16><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
             d_x, d_y, la, teams, threads, w, d_out, s128, ep, (uint32_t)ring);
+      } else {
+        k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
       }
     } else {
       k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
