@@ -141,6 +141,17 @@ int omprt_set_unroll(int unroll);
  * 21-27 = row-group kernels with a forced window size x warps per SM. */
 int omprt_set_variant(int variant);
 
+/* Per-team trace ring — the B200 analog of the vgpu's collect_trace
+ * (vgpu.py:351-353, tgt_target(collect_trace=True) host.py:255-296).  While a
+ * device buffer of `capacity` 32-byte records is installed, every construct
+ * kernel's CTA writes one record {u64 t_begin_ns, u64 t_end_ns, u32 cta,
+ * u32 smid, u32 ticket, u32 kind} at index blockIdx.x: kind 1 = team (ticket
+ * = the value its atom.inc returned), 2 = the last team's ordered combine
+ * (index gridDim.x), 3 = an ORDERED streaming warp (index = warp id, ticket
+ * = groups folded), 4 = the ORDERED folder.  Times are %globaltimer ns.
+ * Pass NULL/0 to uninstall (then kernels write nothing).  Synchronous. */
+int omprt_set_trace(void *d_records, int64_t capacity);
+
 /* Number of streaming multiprocessors of the current device (148 on B200). */
 int omprt_num_sms(void);
 

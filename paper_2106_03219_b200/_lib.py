@@ -58,6 +58,7 @@ _SIGS = {
     "omprt_device_init": ([C.c_int], C.c_int),
     "omprt_set_unroll": ([C.c_int], C.c_int),
     "omprt_set_variant": ([C.c_int], C.c_int),
+    "omprt_set_trace": ([C.c_void_p, C.c_int64], C.c_int),
     "omprt_num_sms": ([], C.c_int),
     "omprt_check_trap": ([C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                           C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),

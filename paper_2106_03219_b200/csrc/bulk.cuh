@@ -276,6 +276,7 @@ template <int STAGES, int STAGE_BYTES, int U>
 __global__ void __launch_bounds__(kMaxThreads)
     k_dot_bulk(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
                Workspace ws, double *out) {
+  trace_begin();
   extern __shared__ __align__(128) unsigned char stages[];
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   if (teams_ticket<OMPRT_OP_ADD, double>(team_val, partials, ws.ticket)) {
     const double v = combine_team_partials<OMPRT_OP_ADD, double>(partials, scratch);
     if (threadIdx.x == 0) *out = *out + v;
+    trace_combine();
   }
 }
 
@@ -313,6 +315,7 @@ template <int STAGES, int STAGE_BYTES, int U, int MAXT = kMaxThreads>
 __global__ void __launch_bounds__(MAXT)
     k_axpy_minmax_bulk(float a, const float *__restrict__ x, float *__restrict__ y, LoopArgs la,
                        Workspace ws, float *out_max, float *out_min) {
+  trace_begin();
   extern __shared__ __align__(128) unsigned char stages[];
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
@@ -352,12 +355,14 @@ __global__ void __launch_bounds__(MAXT)
       *out_max = Red<OMPRT_OP_MAX, float>::apply(*out_max, vmax);
       *out_min = Red<OMPRT_OP_MIN, float>::apply(*out_min, vmin);
     }
+    trace_combine();
   }
 }
 
 template <class T, int OP, int STAGES, int STAGE_BYTES, bool PROXY_FENCE = false>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce_bulk(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
+  trace_begin();
   extern __shared__ __align__(128) unsigned char stages[];
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
@@ -380,6 +385,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   if (teams_ticket<OP, T>(team_val, partials, ws.ticket)) {
     const T v = combine_team_partials<OP, T>(partials, scratch);
     if (threadIdx.x == 0) *out = Red<OP, T>::apply(*out, v);
+    trace_combine();
   }
 }
 

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   __shared__ uint64_t s_off;
   const uint32_t nall = 32u + (uint32_t)P;
   const uint32_t lane = lane_id();
+  trace_begin();
 
   if (warp_id() == 0) {
     // ------------------------------------------------ main warp (sequential part)
@@ -271,7 +272,10 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (lane == 0) {
       partials[blockIdx.x] = team_val;
       fence_acq_rel_gpu();
-      last = atomic_inc_acq_rel_gpu(ws.ticket, gridDim.x - 1) == gridDim.x - 1;
+      const uint32_t t = atomic_inc_acq_rel_gpu(ws.ticket, gridDim.x - 1);
+      last = t == gridDim.x - 1;
+      trace_record(blockIdx.x, kTraceTeam, t, trace_t0());
+      if (last) trace_t0() = globaltimer();
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
@@ -285,6 +289,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         v = warp_reduce<OP, T>(v, 32);
         if (lane == 0 && !trap_raised()) *out = Red<OP, T>::apply(*out, v);
       }
+      trace_combine();
     }
   } else {
     // ------------------------------------------------ worker state machine

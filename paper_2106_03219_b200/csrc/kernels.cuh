@@ -64,11 +64,18 @@ OMPRT_D bool teams_ticket(T team_val, T *partials, uint32_t *ticket) {
     fence_acq_rel_gpu();
     const uint32_t t = atomic_inc_acq_rel_gpu(ticket, gridDim.x - 1);
     s_last = (t == gridDim.x - 1);
+    trace_record(blockIdx.x, kTraceTeam, t, trace_t0());
+    if (s_last) trace_t0() = globaltimer();  // start of the combine
   }
   __syncthreads();
   const bool last = s_last != 0;
   if (last) fence_acq_rel_gpu();
   return last;
+}
+
+// the last team, after writing the result: the combine's trace record
+OMPRT_D void trace_combine() {
+  if (threadIdx.x == 0) trace_record(gridDim.x, kTraceCombine, gridDim.x - 1, trace_t0());
 }
 
 template <int OP, class T>
@@ -293,6 +300,7 @@ OMPRT_D TeamSet team_set_cta(const LoopArgs &la) {
 template <class T, int OP, int U, int LP = kLoadDefault, int VB = 16>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
+  trace_begin();
   __shared__ T scratch[32];
   const TeamSet s = team_set_cta(la);
   ReduceBody<T, OP, LP, VB> body(x);
@@ -302,6 +310,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   if (teams_ticket<OP, T>(team_val, partials, ws.ticket)) {
     const T v = combine_team_partials<OP, T>(partials, scratch);
     if (threadIdx.x == 0) *out = Red<OP, T>::apply(*out, v);
+    trace_combine();
   }
 }
 
@@ -378,6 +387,7 @@ constexpr int kFoldBuf = 2048;  // elements of the static fold buffer
 template <class T, int OP>
 __global__ void __launch_bounds__(kMaxThreads)
     k_reduce_ordered(const T *__restrict__ x, LoopArgs la, Workspace ws, T *out) {
+  trace_begin();
   T part = Red<OP, T>::identity();
   {
     const Bounds bd = schedule_init(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x,
@@ -400,6 +410,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     const T v = fold_in_order_team<OP, T>(threadIdx.x == 0 ? *out : part, tp,
                                           (int64_t)gridDim.x * blockDim.x, buf, kFoldBuf);
     if (threadIdx.x == 0) *out = v;
+    trace_combine();
   }
 }
 
@@ -407,6 +418,7 @@ template <int U>
 __global__ void __launch_bounds__(kMaxThreads)
     k_dot(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la, Workspace ws,
           double *out) {
+  trace_begin();
   __shared__ double scratch[32];
   const TeamSet s = team_set_cta(la);
   DotBody body(x, y);
@@ -416,12 +428,14 @@ __global__ void __launch_bounds__(kMaxThreads)
   if (teams_ticket<OMPRT_OP_ADD, double>(team_val, partials, ws.ticket)) {
     const double v = combine_team_partials<OMPRT_OP_ADD, double>(partials, scratch);
     if (threadIdx.x == 0) *out = *out + v;
+    trace_combine();
   }
 }
 
 __global__ void __launch_bounds__(kMaxThreads)
     k_dot_ordered(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
                   Workspace ws, double *out) {
+  trace_begin();
   double part = 0.0;
   run_thread_chunks(la.sched, la.lb, la.ub, la.chunk,
                     [&](int64_t i) { part = __fma_rn(x[i], y[i], part); });
@@ -433,6 +447,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     const double v = fold_in_order_team<OMPRT_OP_ADD, double>(
         threadIdx.x == 0 ? *out : 0.0, tp, (int64_t)gridDim.x * blockDim.x, buf, kFoldBuf);
     if (threadIdx.x == 0) *out = v;
+    trace_combine();
   }
 }
 
@@ -441,6 +456,7 @@ template <int U>
 __global__ void __launch_bounds__(kMaxThreads)
     k_axpy_minmax(float a, const float *__restrict__ x, float *__restrict__ y, LoopArgs la,
                   Workspace ws, float *out_max, float *out_min) {
+  trace_begin();
   __shared__ float scratch[32];
   const TeamSet s = team_set_cta(la);
   AxpyBody body(a, x, y);
@@ -457,12 +473,14 @@ __global__ void __launch_bounds__(kMaxThreads)
       *out_max = Red<OMPRT_OP_MAX, float>::apply(*out_max, vmax);
       *out_min = Red<OMPRT_OP_MIN, float>::apply(*out_min, vmin);
     }
+    trace_combine();
   }
 }
 
 __global__ void __launch_bounds__(kMaxThreads)
     k_axpy_minmax_ordered(float a, const float *__restrict__ x, float *__restrict__ y,
                           LoopArgs la, Workspace ws, float *out_max, float *out_min) {
+  trace_begin();
   float mx = Limits<float>::lowest(), mn = Limits<float>::highest();
   run_thread_chunks(la.sched, la.lb, la.ub, la.chunk, [&](int64_t i) {
     const float v = __fmaf_rn(a, x[i], y[i]);
@@ -487,6 +505,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       *out_max = vmax;
       *out_min = vmin;
     }
+    trace_combine();
   }
 }
 

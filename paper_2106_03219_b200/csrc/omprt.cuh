@@ -375,6 +375,59 @@ OMPRT_D void raise_trap(int kind, int code) {
 OMPRT_D bool trap_raised() { return *(volatile int *)&g_trap.kind != 0; }
 
 // ---------------------------------------------------------------------------
+// per-team trace ring (the B200 analog of the vgpu's collect_trace,
+// vgpu.py:351-353): when a buffer is installed (omprt_set_trace), thread 0 of
+// every CTA of a construct records when the team started, on which SM, when
+// it took its ticket and which ticket value the atom.inc returned; the last
+// team adds a record for the ordered combine.  One record per CTA, indexed by
+// blockIdx.x (+ gridDim.x for the combine); nothing is written when the
+// buffer is absent (one global load per CTA).
+// ---------------------------------------------------------------------------
+struct TraceRec {
+  uint64_t t_begin, t_end;  // %globaltimer, ns
+  uint32_t cta, smid, ticket, kind;
+};
+enum : uint32_t { kTraceTeam = 1, kTraceCombine = 2, kTraceGroup = 3, kTraceFolder = 4 };
+struct TraceRing {
+  TraceRec *recs;
+  uint32_t cap;
+};
+__device__ TraceRing g_trace;
+
+OMPRT_D uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+OMPRT_D uint32_t smid() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+OMPRT_D uint64_t &trace_t0() {
+  __shared__ uint64_t t0;
+  return t0;
+}
+// thread 0, at the top of a construct kernel
+OMPRT_D void trace_begin() {
+  if (threadIdx.x == 0 && g_trace.recs) trace_t0() = globaltimer();
+}
+// thread 0: record slot `slot` (CTA index, or gridDim.x + k for extras)
+OMPRT_D void trace_record(uint32_t slot, uint32_t kind, uint32_t ticket, uint64_t t0) {
+  const TraceRing r = g_trace;
+  if (r.recs && slot < r.cap) {
+    TraceRec rec;
+    rec.t_begin = t0;
+    rec.t_end = globaltimer();
+    rec.cta = blockIdx.x;
+    rec.smid = smid();
+    rec.ticket = ticket;
+    rec.kind = kind;
+    r.recs[slot] = rec;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // team reductions: warp __shfl_xor_sync tree, then a shared-memory tree over
 // the warps (__kmpc_nvptx_parallel_reduce_nowait_v2).  Handles a partial last
 // warp (threads not a multiple of 32).  The result is valid in thread 0.

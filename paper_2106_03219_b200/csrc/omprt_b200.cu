@@ -455,6 +455,16 @@ int omprt_device_init(int device) {
   return OMPRT_OK;
 }
 
+int omprt_set_trace(void *d_records, int64_t capacity) {
+  if (capacity < 0 || (capacity > 0 && !d_records))
+    return fail(OMPRT_EINVAL, "set_trace: bad arguments");
+  TraceRing r;
+  r.recs = capacity > 0 ? reinterpret_cast<TraceRec *>(d_records) : nullptr;
+  r.cap = (uint32_t)(capacity > 0xffffffffll ? 0xffffffffll : capacity);
+  OMPRT_CUDA(cudaMemcpyToSymbol(g_trace, &r, sizeof(r)));
+  return OMPRT_OK;
+}
+
 int omprt_num_sms(void) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(OMPRT_ECUDA, "no CUDA device");

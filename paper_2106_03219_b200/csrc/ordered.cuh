@@ -230,8 +230,9 @@ OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
   T *tiles = (T *)(base + L::kTable);
   const int64_t P = teams * threads;
   const int64_t ngroups = (P + 31) / 32;
+  uint32_t ndone = 0;
   for (int64_t grp = (int64_t)blockIdx.x * nwarps + warp; grp < ngroups;
-       grp += (int64_t)gridDim.x * nwarps) {
+       grp += (int64_t)gridDim.x * nwarps, ++ndone) {
     OrdRow<W, V> ld, fd;
     ld.init(la, grp * 32 + lane, teams, threads);
     fd = ld;
@@ -265,6 +266,9 @@ OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
     __syncwarp();
     if (lane == 0) st_release_gpu(flags + grp, epoch);
   }
+  // trace: one record per streaming warp (groups it folded), slot = warp id
+  if (lane == 0)
+    trace_record(blockIdx.x * nwarps + warp, kTraceGroup, ndone, trace_t0());
 }
 
 // Load V elements (16 bytes) of a shared-memory row.
@@ -386,7 +390,10 @@ OMPRT_D void ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t 
     }
     __syncwarp();
   }
-  if (lane == 0) *out = acc;
+  if (lane == 0) {
+    *out = acc;
+    trace_record(gridDim.x * ((blockDim.x >> 5) - 1), kTraceFolder, (uint32_t)nb, trace_t0());
+  }
 }
 
 template <int OP, class T> struct RedComb {
@@ -406,6 +413,8 @@ template <class T, int OP, int W>
 __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
     k_reduce_ordered_rows(const T *__restrict__ x, LoopArgs la, int teams, int threads,
                           Workspace ws, T *out, int stages, uint64_t epoch, uint32_t ring_off) {
+  trace_begin();
+  __syncthreads();  // the CTA's trace start time, read by every warp at its end
   const int64_t P = (int64_t)teams * threads;
   T *tp = (T *)ws.thread_partials;
   uint64_t *flags = (uint64_t *)(ws.thread_partials + ord_flags_offset(P));
@@ -425,6 +434,8 @@ __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
     k_dot_ordered_rows(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
                        int teams, int threads, Workspace ws, double *out, int stages,
                        uint64_t epoch, uint32_t ring_off) {
+  trace_begin();
+  __syncthreads();  // the CTA's trace start time, read by every warp at its end
   const int64_t P = (int64_t)teams * threads;
   double *tp = (double *)ws.thread_partials;
   uint64_t *flags = (uint64_t *)(ws.thread_partials + ord_flags_offset(P));

@@ -292,7 +292,7 @@ def b200_tgt_target(call, bundle, device="vgpu", force_fail: bool = False, *, gr
         return 1
     teams, threads = grid if grid is not None else (call.grid[0] or 1, call.grid[1] or 1)
     if FAST_PATH and not check_uninit:
-        st = _run_recognised(call, teams, threads, out)
+        st = _run_recognised(call, teams, threads, out, collect_trace)
         if st is not None:
             return st
     image = image_for(bundle, call)
@@ -301,7 +301,8 @@ def b200_tgt_target(call, bundle, device="vgpu", force_fail: bool = False, *, gr
     return _run_image(image, call, teams, threads, check_uninit, out)
 
 
-def _run_recognised(call, teams: int, threads: int, out: dict | None) -> int | None:
+def _run_recognised(call, teams: int, threads: int, out: dict | None,
+                    collect_trace: bool = False) -> int | None:
     """The reduction idiom as one omprt_reduce construct launch, or None."""
     from forge import host as H
 
@@ -351,12 +352,19 @@ def _run_recognised(call, teams: int, threads: int, out: dict | None) -> int | N
         # an idempotent combine of the per-thread start value (max/min)
         out_dev.copy_(torch.from_numpy(np.array(
             [runtime_fold(plan.op, int(out_dev.cpu().item()), init, plan.elem)], dtype=dt)))
-    runtime.reduce(x, plan.op, lb=lb, ub=ub, sched="static", teams=teams, threads=threads,
-                   out=out_dev)
+    tracer = runtime.Trace(dev) if collect_trace else None
+    if tracer is not None:
+        tracer.__enter__()
+    try:
+        runtime.reduce(x, plan.op, lb=lb, ub=ub, sched="static", teams=teams, threads=threads,
+                       out=out_dev)
+    finally:
+        if tracer is not None:
+            tracer.__exit__(None, None, None)
     torch.cuda.synchronize(dev)
     if out is not None:
         out["result"] = None
-        out["trace"] = []
+        out["trace"] = tracer.lines() if tracer is not None else []
     H._write_back(vals[plan.cell], cell.cpu().numpy().tobytes())
     return 0
 

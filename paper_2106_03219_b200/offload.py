@@ -207,8 +207,11 @@ def tgt_target(call: TargetCall, bundle, device="b200", force_fail: bool = False
 
     bundle: {"b200": {kernel_id: RegionKernel}}.  On 0 the buffer arguments
     hold the device results; on nonzero status they are untouched.
-    sched_seed / check_uninit / collect_trace are accepted for signature
-    compatibility (hardware scheduling has no seed).
+    sched_seed / check_uninit are accepted for signature compatibility
+    (hardware scheduling has no seed).  collect_trace=True
+    records the construct's per-team device trace (runtime.Trace) into
+    out["trace"] — team start/SM, the ticket each team's atom.inc took, the
+    ordered combine — in the vgpu's "seq team thread kind detail" format.
     """
     if call.values is None:
         raise ValueError("TargetCall is not bound to argument values")
@@ -243,6 +246,31 @@ def tgt_target(call: TargetCall, bundle, device="b200", force_fail: bool = False
     r = rk.roles
     c = rk.construct
     st = torch.cuda.current_stream(dev)
+    tracer = runtime.Trace(dev) if (collect_trace and c != "bounds") else None
+    if tracer is not None:
+        tracer.__enter__()
+    try:
+        _launch_construct(rk, c, r, scal, dbufs, teams, threads, dev)
+    finally:
+        if tracer is not None:
+            tracer.__exit__(None, None, None)
+
+    trap = runtime.check_trap(dev)  # synchronises the stream
+    st.synchronize()
+    if out is not None:
+        out["result"] = {"construct": c, "teams": teams, "threads": threads}
+        out["trace"] = tracer.lines() if tracer is not None else []
+    if trap is not None:
+        return _trap_status(trap, out)
+    # copy-out only on status 0 (host.py:293-295)
+    for name, (d, v) in by_name.items():
+        if d.kind == "buffer":
+            _write_back(d, v, dbufs[name])
+    return 0
+
+
+def _launch_construct(rk: RegionKernel, c: str, r: dict, scal: dict, dbufs: dict, teams: int,
+                      threads: int, dev: torch.device) -> None:
     if c == "reduce":
         n = int(scal[r["n"]])
         runtime.reduce(dbufs[r["x"]], rk.op, lb=rk.lb, ub=rk.lb + n - 1, sched=rk.sched,
@@ -273,18 +301,6 @@ def tgt_target(call: TargetCall, bundle, device="b200", force_fail: bool = False
         dbufs[r["out"]].copy_(res.reshape(-1)[: dbufs[r["out"]].numel()])
     else:
         raise ValueError(f"unknown construct '{c}'")
-
-    trap = runtime.check_trap(dev)  # synchronises the stream
-    st.synchronize()
-    if out is not None:
-        out["result"] = {"construct": c, "teams": teams, "threads": threads}
-    if trap is not None:
-        return _trap_status(trap, out)
-    # copy-out only on status 0 (host.py:293-295)
-    for name, (d, v) in by_name.items():
-        if d.kind == "buffer":
-            _write_back(d, v, dbufs[name])
-    return 0
 
 
 def _launch_compiled(image, call: TargetCall, grid, check_uninit: bool, out) -> int:

@@ -19,8 +19,11 @@ Names follow the OpenMP device runtime the paper rewrites:
 from __future__ import annotations
 
 import ctypes as C
+import functools
+import os
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -149,6 +152,87 @@ def bounds_dump(lb: int, ub: int, sched="static", chunk: int = 1, *, teams: int,
     return out
 
 
+# ------------------------------------------------------------- NVTX ranges
+
+_NVTX = os.environ.get("OMPRT_NVTX", "") not in ("", "0")
+
+
+def _nvtx(name: str):
+    """With OMPRT_NVTX=1 every construct launch is an NVTX range (for Nsight
+    Systems timelines); otherwise the function is returned untouched."""
+    def deco(fn):
+        if not _NVTX:
+            return fn
+
+        @functools.wraps(fn)
+        def wrapped(*a, **k):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*a, **k)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrapped
+    return deco
+
+
+# ------------------------------------------------------------- trace ring
+
+TRACE_REC = np.dtype([("t_begin", "<u8"), ("t_end", "<u8"), ("cta", "<u4"), ("smid", "<u4"),
+                      ("ticket", "<u4"), ("kind", "<u4")])
+TRACE_KINDS = {1: "atomic.inc", 2: "combine", 3: "stream", 4: "fold"}
+
+
+class Trace:
+    """Per-team device trace of the constructs launched inside the block —
+    the B200 analog of the vgpu's collect_trace (vgpu.py:351-353).  Every CTA
+    of a construct records when it started, on which SM, when it took its
+    last-team-finishes ticket and the ticket value its atom.inc returned; the
+    last team records the ordered combine; ORDERED launches record each
+    streaming warp and the folder.  `lines()` renders them like the vgpu's
+    trace ("seq team thread kind detail"), ordered by completion time.
+    One construct per Trace (records are indexed by CTA)."""
+
+    def __init__(self, device: torch.device | None = None, capacity: int = 16384):
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.capacity = capacity
+        self.buf = torch.zeros(capacity * TRACE_REC.itemsize // 8, dtype=torch.int64,
+                               device=self.device)
+        self.records = np.zeros(0, dtype=TRACE_REC)
+
+    def __enter__(self):
+        torch.cuda.synchronize(self.device)
+        check(_lib.load().omprt_set_trace(_p(self.buf), self.capacity), "omprt_set_trace")
+        return self
+
+    def __exit__(self, *exc):
+        torch.cuda.synchronize(self.device)
+        check(_lib.load().omprt_set_trace(None, 0), "omprt_set_trace")
+        raw = self.buf.cpu().numpy().view(np.uint8).view(TRACE_REC)
+        self.records = raw[raw["kind"] != 0].copy()
+        return False
+
+    def lines(self) -> list[str]:
+        r = np.sort(self.records, order="t_end")
+        if r.size == 0:
+            return []
+        t0 = int(r["t_begin"][r["t_begin"] > 0].min()) if (r["t_begin"] > 0).any() else 0
+        out = []
+        for seq, rec in enumerate(r):
+            kind = TRACE_KINDS.get(int(rec["kind"]), f"kind{int(rec['kind'])}")
+            b, e = int(rec["t_begin"]) - t0, int(rec["t_end"]) - t0
+            if kind == "atomic.inc":
+                detail = (f"ticket old={int(rec['ticket'])} sm={int(rec['smid'])} "
+                          f"begin_ns={b} end_ns={e}")
+            elif kind == "combine":
+                detail = f"teams={int(rec['ticket']) + 1} begin_ns={b} end_ns={e}"
+            elif kind == "stream":
+                detail = f"groups={int(rec['ticket'])} sm={int(rec['smid'])} end_ns={e}"
+            else:
+                detail = f"batches={int(rec['ticket'])} end_ns={e}"
+            out.append(f"{seq} {int(rec['cta'])} 0 {kind} {detail}")
+        return out
+
+
 # ------------------------------------------------------------- workspace
 
 _ws_cache: dict[tuple, torch.Tensor] = {}
@@ -172,6 +256,7 @@ def reduce_workspace(device: torch.device, teams: int, threads: int, mode: int) 
 
 # ---------------------------------------------------------------- reduce
 
+@_nvtx("omprt_reduce")
 def reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = None, sched="static",
            chunk: int = 1, teams: int | None = None, threads: int | None = None, mode="spmd",
            out: torch.Tensor | None = None, init=None) -> torch.Tensor:
@@ -203,6 +288,7 @@ def reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = None, sch
     return out
 
 
+@_nvtx("omprt_axpy_minmax")
 def axpy_minmax(a: float, x: torch.Tensor, y: torch.Tensor, *, lb: int = 0, ub: int | None = None,
                 sched="distribute_chunked", chunk: int = 1, teams: int | None = None,
                 threads: int | None = None, mode="spmd",
@@ -230,6 +316,7 @@ def axpy_minmax(a: float, x: torch.Tensor, y: torch.Tensor, *, lb: int = 0, ub: 
     return out_max, out_min
 
 
+@_nvtx("omprt_dot")
 def dot(x: torch.Tensor, y: torch.Tensor, *, lb: int = 0, ub: int | None = None,
         sched="static", chunk: int = 1, teams: int | None = None, threads: int | None = None,
         mode="spmd", out: torch.Tensor | None = None) -> torch.Tensor:
@@ -265,6 +352,7 @@ def combine_partials(partials: torch.Tensor, op="add", out: torch.Tensor | None 
 
 # -------------------------------------------------------------- generic
 
+@_nvtx("omprt_generic_reduce")
 def generic_reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = None,
                    teams: int = 1024, par_threads: int = 256, ordered: bool = False,
                    pad_bytes: int = 0, heap_fallback: bool = False,
