@@ -135,3 +135,19 @@ def test_forge_reduction_regions_on_b200(cuda, fallback_golden):
             assert int(got) == r["fallback"], r
     finally:
         B.uninstall()
+
+
+@pytest.mark.gpu
+def test_forge_collect_trace_on_b200(cuda):
+    # forge's own run_source(collect_trace=True) on device "b200": the
+    # recognised reduction region returns the per-team hardware trace in the
+    # vgpu's line format ("seq team thread kind detail")
+    B.install()
+    try:
+        src = dict(corpus.CORPUS)["partial_sums"]
+        res = run_source(src, device="b200", collect_trace=True)
+        assert res.exit_status == 0
+        kinds = [ln.split()[3] for ln in res.device_traces]
+        assert "atomic.inc" in kinds and kinds[-1] == "combine"
+    finally:
+        B.uninstall()
