@@ -171,6 +171,23 @@ inline int ord_default_nw(int teams, int threads) {
   return (int)(nw < 1 ? 1 : (nw > 8 ? 8 : nw));
 }
 
+// Segments per group for the dynamic (load-balanced) ORDERED walk: block
+// schedules only, ~64+ windows per unit, at most 8 units per group;
+// omprt_set_variant(31) keeps the static assignment.
+constexpr int kOrderedStatic = 31;
+
+int ord_segments(const LoopArgs &la, int teams, int threads, int window_elems) {
+  if (g_variant == kOrderedStatic) return 0;
+  if (la.sched == OMPRT_SCHED_STATIC_CHUNKED || la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED)
+    return 0;
+  if (la.ub < la.lb) return 0;
+  const int64_t P = (int64_t)teams * threads;
+  const int64_t per_row = (la.ub - la.lb + 1 + P - 1) / P;
+  const int64_t windows = per_row / window_elems;
+  int64_t seg = windows / 64;
+  return (int)(seg < 1 ? 1 : (seg > 8 ? 8 : seg));
+}
+
 template <class T, int OP, int WB>
 int launch_ordered_rows(const T *xp, LoopArgs la, int teams, int threads, int nw, Workspace w,
                         T *op, cudaStream_t st) {
@@ -184,7 +201,8 @@ int launch_ordered_rows(const T *xp, LoopArgs la, int teams, int threads, int nw
   int rc = set_smem(kern, smem);
   if (rc) return rc;
   kern<<<ord_grid(teams, threads, nw), (nw + 1) * 32, smem, st>>>(
-      xp, la, teams, threads, w, op, stages, next_epoch(), (uint32_t)ring);
+      xp, la, teams, threads, w, op, stages, next_epoch(), (uint32_t)ring,
+      ord_segments(la, teams, threads, W));
   return check_launch("omprt_reduce(ordered rows)");
 }
 
@@ -591,19 +609,22 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
         const size_t smem = ring + kFolderSmem;
         if ((rc = set_smem(k_dot_ordered_rows<64>, smem))) return rc;
         k_dot_ordered_rows<64><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
-            d_x, d_y, la, teams, threads, w, d_out, s512, ep, (uint32_t)ring);
+            d_x, d_y, la, teams, threads, w, d_out, s512, ep, (uint32_t)ring,
+            ord_segments(la, teams, threads, 64));
       } else if (s256 >= 2) {
         const size_t ring = (size_t)nw * OrdSmem<double, 32, 2>::warp_bytes(s256);
         const size_t smem = ring + kFolderSmem;
         if ((rc = set_smem(k_dot_ordered_rows<32>, smem))) return rc;
         k_dot_ordered_rows<32><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
-            d_x, d_y, la, teams, threads, w, d_out, s256, ep, (uint32_t)ring);
+            d_x, d_y, la, teams, threads, w, d_out, s256, ep, (uint32_t)ring,
+            ord_segments(la, teams, threads, 32));
       } else if (s128 >= 2) {
         const size_t ring = (size_t)nw * OrdSmem<double, 16, 2>::warp_bytes(s128);
         const size_t smem = ring + kFolderSmem;
         if ((rc = set_smem(k_dot_ordered_rows<16>, smem))) return rc;
         k_dot_ordered_rows<16><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
-            d_x, d_y, la, teams, threads, w, d_out, s128, ep, (uint32_t)ring);
+            d_x, d_y, la, teams, threads, w, d_out, s128, ep, (uint32_t)ring,
+            ord_segments(la, teams, threads, 16));
       } else {
         k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
       }

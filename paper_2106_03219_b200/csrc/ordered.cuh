@@ -85,9 +85,11 @@ template <int W, int V> struct OrdRow {
   int64_t hi;  // current chunk end (inclusive)
   int64_t a;   // current window start (V-aligned, a <= p)
   int64_t clo, stride, limit, chunk;
+  int64_t left;  // windows this cursor may still take (segmented walks)
   bool chunked;
 
   OMPRT_D void init(const LoopArgs &la, int64_t g, int64_t teams, int64_t threads) {
+    left = INT64_MAX;
     chunked = (la.sched == OMPRT_SCHED_STATIC_CHUNKED ||
                la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED);
     if (g >= teams * threads) {  // lane past the last OpenMP thread: dead row
@@ -112,13 +114,24 @@ template <int W, int V> struct OrdRow {
     }
     a = p & ~(int64_t)(V - 1);
   }
-  OMPRT_D bool live() const { return p <= hi; }
+  OMPRT_D bool live() const { return p <= hi && left > 0; }
+  // windows of a (non-chunked) row, and positioning at window w0 with a
+  // budget of n windows: segment s of a row is windows [s*K, s*K + K)
+  OMPRT_D int64_t windows() const { return p <= hi ? (hi - a) / W + 1 : 0; }
+  OMPRT_D void seek(int64_t w0, int64_t n) {
+    if (w0 > 0) {
+      a += w0 * W;
+      p = a;
+    }
+    left = n;
+  }
   // the current window's fold range as offsets from a: [s, e]
   OMPRT_D int s() const { return (int)(p - a); }
   OMPRT_D int e() const { return (int)((hi - a) < (W - 1) ? (hi - a) : (W - 1)); }
   OMPRT_D void advance() {
     a += W;
     p = a;
+    --left;
     if (p > hi && chunked) {
       clo += stride;
       if (clo <= limit) {
@@ -212,14 +225,24 @@ OMPRT_D void ord_issue(OrdRow<W, 16 / sizeof(T)> &row, const T *const (&src)[NS]
   if (live) row.advance();
 }
 
-// Stream this warp's groups through the ring; fold(rows, s, e) consumes this
+// Stream this warp's work through the ring; fold(rows, s, e) consumes this
 // lane's row offsets s..e of the current tile in order, fold.publish(g)
-// stores OpenMP thread g's partial; then flags[grp] = epoch announces the
-// group's 32 partials to the folder.
+// stores OpenMP thread g's running partial (fold.resume(g) reloads it).
+//
+// seg == 0 (static): warp w takes groups w, w + all warps, ... whole, then
+// flags[grp] = epoch announces the group's 32 final partials to the folder.
+// seg > 0 (dynamic, block schedules): the work is seg × ngroups units
+// (segment s of group g = windows [s*K, s*K+K) of its rows), claimed in
+// segment-major order from a self-resetting atom.inc counter (the ticket
+// word), so SMs that stream faster take more units.  Unit (g, s) waits for
+// flags[g] == epoch + s (segment s-1 done), resumes the 32 running partials,
+// and leaves flags[g] = epoch + s + 1; the folder waits for epoch + seg.
+// The dependency always points at an earlier-claimed unit held by a running
+// warp, so the chain terminates at s = 0 (no deadlock).
 template <class T, int W, int NS, class Fold>
 OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
                         const T *const (&src)[NS], int stages, Fold &fold, uint64_t *flags,
-                        uint64_t epoch) {
+                        uint64_t epoch, int seg, uint32_t *counter) {
   using L = OrdSmem<T, W, NS>;
   constexpr int V = L::V;
   extern __shared__ __align__(16) unsigned char ord_smem[];
@@ -230,11 +253,53 @@ OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
   T *tiles = (T *)(base + L::kTable);
   const int64_t P = teams * threads;
   const int64_t ngroups = (P + 31) / 32;
+  const int64_t units = seg > 0 ? (int64_t)seg * ngroups : ngroups;
+  const uint32_t bound = (uint32_t)(units + (int64_t)gridDim.x * nwarps - 1);
   uint32_t ndone = 0;
-  for (int64_t grp = (int64_t)blockIdx.x * nwarps + warp; grp < ngroups;
-       grp += (int64_t)gridDim.x * nwarps, ++ndone) {
+  int64_t next = (int64_t)blockIdx.x * nwarps + warp;  // static scheme
+  for (;; ++ndone) {
+    int64_t u;
+    if (seg > 0) {
+      uint32_t t = 0;
+      if (lane == 0) t = atomic_inc_acq_rel_gpu(counter, bound);
+      u = (int64_t)__shfl_sync(0xffffffffu, t, 0);
+    } else {
+      u = next;
+      next += (int64_t)gridDim.x * nwarps;
+    }
+    if (u >= units) break;
+    // dynamic order: waves of `wave` groups (one per streaming warp of the
+    // grid), segment-major inside a wave, so groups still complete wave by
+    // wave for the folder
+    int64_t grp = u;
+    int sidx = 0;
+    if (seg > 0) {
+      const int64_t wave = (int64_t)gridDim.x * nwarps;
+      const int64_t per_wave = wave * seg;
+      const int64_t wv = u / per_wave, r = u - wv * per_wave;
+      const int64_t g0 = wv * wave;
+      const int64_t gw = (ngroups - g0) < wave ? (ngroups - g0) : wave;  // groups in this wave
+      sidx = (int)(r / gw);
+      grp = g0 + r % gw;
+    }
+    const int64_t g = grp * 32 + lane;
     OrdRow<W, V> ld, fd;
-    ld.init(la, grp * 32 + lane, teams, threads);
+    ld.init(la, g, teams, threads);
+    if (seg > 0) {
+      const uint32_t nwin = (uint32_t)ld.windows();
+      const int64_t gmax = (int64_t)__reduce_max_sync(0xffffffffu, nwin);
+      const int64_t K = (gmax + seg - 1) / seg, w0 = (int64_t)sidx * K;
+      int64_t n = (int64_t)nwin - w0;
+      n = n < 0 ? 0 : (n > K ? K : n);
+      ld.seek(w0, n);
+      if (sidx > 0) {
+        if (lane == 0)
+          while (ld_acquire_gpu(flags + grp) != epoch + (uint64_t)sidx) {
+          }
+        __syncwarp();
+        if (g < P) fold.resume(g);
+      }
+    }
     fd = ld;
     for (int s = 0; s + 1 < stages; ++s)
       ord_issue<T, W, NS>(ld, src, la.lb, la.ub, table, tiles, s, lane);
@@ -260,13 +325,13 @@ OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
     }
     cp_async_wait(0);
     __syncwarp();
-    if (grp * 32 + lane < P) fold.publish(grp * 32 + lane);
-    // group ready: the lanes' partials, then the flag (release, gpu scope)
+    if (g < P) fold.publish(g);
+    // the lanes' partials, then the flag (release, gpu scope)
     __threadfence();
     __syncwarp();
-    if (lane == 0) st_release_gpu(flags + grp, epoch);
+    if (lane == 0) st_release_gpu(flags + grp, epoch + (uint64_t)(seg > 0 ? sidx + 1 : 0));
   }
-  // trace: one record per streaming warp (groups it folded), slot = warp id
+  // trace: one record per streaming warp (units it folded), slot = warp id
   if (lane == 0)
     trace_record(blockIdx.x * nwarps + warp, kTraceGroup, ndone, trace_t0());
 }
@@ -300,6 +365,7 @@ template <class T, int OP, int W> struct OrdReduceFold {
     tp[g] = part;
     part = Red<OP, T>::identity();
   }
+  OMPRT_D void resume(int64_t g) { part = ld_cg(tp + g); }
 };
 
 template <int W> struct OrdDotFold {
@@ -324,6 +390,7 @@ template <int W> struct OrdDotFold {
     tp[g] = part;
     part = 0.0;
   }
+  OMPRT_D void resume(int64_t g) { part = ld_cg(tp + g); }
 };
 
 // The folder: one warp (the extra warp of CTA 0) folds the P per-thread
@@ -412,7 +479,8 @@ constexpr int kOrdMaxWarps = 16;  // streaming warps per CTA (+1 folder warp)
 template <class T, int OP, int W>
 __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
     k_reduce_ordered_rows(const T *__restrict__ x, LoopArgs la, int teams, int threads,
-                          Workspace ws, T *out, int stages, uint64_t epoch, uint32_t ring_off) {
+                          Workspace ws, T *out, int stages, uint64_t epoch, uint32_t ring_off,
+                          int seg) {
   trace_begin();
   __syncthreads();  // the CTA's trace start time, read by every warp at its end
   const int64_t P = (int64_t)teams * threads;
@@ -421,19 +489,20 @@ __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
   if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
     extern __shared__ __align__(16) unsigned char ord_smem[];
     if (blockIdx.x == 0)
-      ord_folder<OP, T>(tp, P, flags, epoch, out, (T *)(ord_smem + ring_off), RedComb<OP, T>());
+      ord_folder<OP, T>(tp, P, flags, epoch + (uint64_t)seg, out, (T *)(ord_smem + ring_off),
+                        RedComb<OP, T>());
     return;
   }
   OrdReduceFold<T, OP, W> f{Red<OP, T>::identity(), tp};
   const T *src[1] = {x};
-  ord_groups<T, W, 1>(la, teams, threads, src, stages, f, flags, epoch);
+  ord_groups<T, W, 1>(la, teams, threads, src, stages, f, flags, epoch, seg, ws.ticket);
 }
 
 template <int W>
 __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
     k_dot_ordered_rows(const double *__restrict__ x, const double *__restrict__ y, LoopArgs la,
                        int teams, int threads, Workspace ws, double *out, int stages,
-                       uint64_t epoch, uint32_t ring_off) {
+                       uint64_t epoch, uint32_t ring_off, int seg) {
   trace_begin();
   __syncthreads();  // the CTA's trace start time, read by every warp at its end
   const int64_t P = (int64_t)teams * threads;
@@ -442,13 +511,14 @@ __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
   if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
     extern __shared__ __align__(16) unsigned char ord_smem[];
     if (blockIdx.x == 0)
-      ord_folder<OMPRT_OP_ADD, double>(tp, P, flags, epoch, out, (double *)(ord_smem + ring_off),
+      ord_folder<OMPRT_OP_ADD, double>(tp, P, flags, epoch + (uint64_t)seg, out,
+                                       (double *)(ord_smem + ring_off),
                                        RedComb<OMPRT_OP_ADD, double>());
     return;
   }
   OrdDotFold<W> f{0.0, tp};
   const double *src[2] = {x, y};
-  ord_groups<double, W, 2>(la, teams, threads, src, stages, f, flags, epoch);
+  ord_groups<double, W, 2>(la, teams, threads, src, stages, f, flags, epoch, seg, ws.ticket);
 }
 
 // Host side: can the row-group kernels take this launch?  x (and y) must be

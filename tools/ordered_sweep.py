@@ -16,7 +16,7 @@ for sched, chunk, teams, threads in (("distribute", 1, 148, 256), ("distribute",
                                      ("distribute", 1, 148, 128), ("distribute", 1, 296, 256),
                                      ("static_chunked", 64, 148, 256)):
     ref = None
-    for var in (20, 0, 21, 22, 23, 24, 25, 26, 27):
+    for var in (20, 31, 0, 21, 22, 23, 24, 25, 26, 27):
         runtime.set_variant(var)
         out = torch.zeros(1, dtype=torch.float64, device=dev)
 
