@@ -1,0 +1,90 @@
+"""The multi-GPU path end to end on the device: 2 ranks (processes) sharing
+cuda:0 over gloo run parallel.reduce_sharded / dot_sharded — each rank's
+shard through the real kernels, then the collective and the rank-ordered
+device combine — and must reproduce the single-launch result (integers:
+bit-exact; fp64: the exact sum within 1e-6, identical bits on both ranks).
+The 8-GPU NCCL run is the bench's; this checks the plumbing on one GPU.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank: int, world: int, port: int, q) -> None:
+    from paper_2106_03219_b200 import parallel, runtime
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        n = 3_000_017
+        lo, hi = parallel.shard(0, n - 1, rank, world)
+        res = {}
+        xi = runtime.synthetic(hi - lo + 1, "i64", O.SEED, 0, offset=lo, device=dev)
+        out = torch.zeros(1, dtype=torch.int64, device=dev)
+        parallel.reduce_sharded(xi, "add", out=out, sched="distribute", teams=37, threads=256)
+        res["i64_sum"] = int(out.item())
+        outm = torch.full((1,), np.iinfo(np.int64).min, dtype=torch.int64, device=dev)
+        parallel.reduce_sharded(xi, "max", out=outm, teams=16, threads=128)
+        res["i64_max"] = int(outm.item())
+        xf = runtime.synthetic(hi - lo + 1, "f64", O.SEED, 0, offset=lo, device=dev)
+        of = torch.zeros(1, dtype=torch.float64, device=dev)
+        parallel.reduce_sharded(xf, "add", out=of, sched="distribute", teams=64, threads=256)
+        res["f64_sum"] = float(of.item())
+        yf = runtime.synthetic(hi - lo + 1, "f64", O.SEED, 1, offset=lo, device=dev)
+        od = torch.zeros(1, dtype=torch.float64, device=dev)
+        parallel.dot_sharded(xf, yf, out=od, deterministic=True)
+        res["dot"] = float(od.item())
+        torch.cuda.synchronize()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_reduce_and_dot_two_ranks_one_gpu(cuda):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = 3_000_017
+    want_sum = O.reduce_flat_gen(0, n - 1, O.I64, O.ADD)
+    want_max = O.reduce_flat_gen(0, n - 1, O.I64, O.MAX, init=np.iinfo(np.int64).min)
+    exact = O.exact_sum_gen(0, n - 1, O.F64)
+    dot_truth = O.accurate_dot_gen(0, n - 1)
+    for r in range(world):
+        assert got[r]["i64_sum"] == int(want_sum)
+        assert got[r]["i64_max"] == int(want_max)
+        assert abs(got[r]["f64_sum"] - exact) <= 1e-6 * exact
+        assert abs(got[r]["dot"] - dot_truth) <= 1e-6 * dot_truth
+    # the deterministic (rank-ordered) combines leave identical bits on every rank
+    assert got[0]["f64_sum"] == got[1]["f64_sum"]
+    assert got[0]["dot"] == got[1]["dot"]
