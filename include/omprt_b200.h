@@ -78,7 +78,8 @@ enum omprt_status {
   OMPRT_TRAP = 2,
   OMPRT_EINVAL = -1,
   OMPRT_ECUDA = -2,
-  OMPRT_ENOMEM = -3
+  OMPRT_ENOMEM = -3,
+  OMPRT_EUNAVAILABLE = -4  /* a runtime dependency (NCCL) is not installed */
 };
 
 enum omprt_trap_kind {
@@ -142,6 +143,17 @@ int omprt_set_unroll(int unroll);
  * 30 = SPMD without splitting few teams over several CTAs; 31 = ORDERED
  * row-group kernels with the static group assignment (no dynamic segments). */
 int omprt_set_variant(int variant);
+
+/* One in-place all-reduce of `count` elements of d_buf over an NCCL
+ * communicator (`nccl_comm` = an ncclComm_t): the combine of the per-GPU
+ * partials of a sharded construct (the GPU level of the
+ * static_bounds partition).  Integer sums are reduced as unsigned (wrap
+ * mod 2^n like the reference's adds), max/min as signed.  NCCL is loaded at
+ * first use (dlopen libnccl.so.2: the instance the communicator came from
+ * when it is already loaded); OMPRT_EUNAVAILABLE without it.  Stream-ordered.
+ * Python callers use torch.distributed (paper_2106_03219_b200.parallel). */
+int omprt_allreduce(void *d_buf, int64_t count, int dtype, int op, void *nccl_comm,
+                    void *stream);
 
 /* Per-team trace ring — the B200 analog of the vgpu's collect_trace
  * (vgpu.py:351-353, tgt_target(collect_trace=True) host.py:255-296).  While a

@@ -23,7 +23,7 @@ MODE_SPMD, MODE_ORDERED = range(2)
 ATOMIC_ADD, ATOMIC_MAX, ATOMIC_MIN, ATOMIC_XCHG, ATOMIC_CAS, ATOMIC_INC = range(6)
 ARENA_ALLOC, ARENA_FREE, ARENA_WRITE, ARENA_READ = range(4)
 OK, FALLBACK, TRAP = 0, 1, 2
-EINVAL, ECUDA, ENOMEM = -1, -2, -3
+EINVAL, ECUDA, ENOMEM, EUNAVAILABLE = -1, -2, -3, -4
 ARENA_CAPACITY = 65536
 ARENA_ALIGN = 8
 
@@ -59,6 +59,8 @@ _SIGS = {
     "omprt_set_unroll": ([C.c_int], C.c_int),
     "omprt_set_variant": ([C.c_int], C.c_int),
     "omprt_set_trace": ([C.c_void_p, C.c_int64], C.c_int),
+    "omprt_allreduce": ([C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p],
+                        C.c_int),
     "omprt_num_sms": ([], C.c_int),
     "omprt_check_trap": ([C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                           C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),

@@ -2,6 +2,7 @@
 // Single translation unit: the device runtime, every kernel and the host
 // entry points, so the trap word is one device symbol.
 #include <atomic>
+#include <dlfcn.h>
 #include <chrono>
 #include <unistd.h>
 #include <cstdarg>
@@ -470,6 +471,57 @@ int omprt_device_init(int device) {
   OMPRT_CUDA(cudaSetDevice(device));
   TrapWord z = {0, 0, 0, 0};
   OMPRT_CUDA(cudaMemcpyToSymbol(g_trap, &z, sizeof(z)));
+  return OMPRT_OK;
+}
+
+// ------------------------------------------------------- multi-GPU combine
+//
+// One in-place NCCL all-reduce of the per-GPU partials.  NCCL
+// is resolved at first use with dlopen("libnccl.so.2") — the library the
+// caller's communicator came from when it is already loaded (torch's, or the
+// system one) — so libomprt_b200.so has no link-time NCCL dependency.
+// Integer sums travel as unsigned (two's-complement wrap, the reference's
+// modular adds); max/min keep the signed type (signed compare).
+namespace {
+using nccl_allreduce_fn = int (*)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+nccl_allreduce_fn g_nccl_allreduce = nullptr;
+std::mutex g_nccl_mu;
+
+int nccl_dtype(int dtype, int op) {
+  const bool add = op == OMPRT_OP_ADD;
+  switch (dtype) {
+    case OMPRT_I32: return add ? 3 : 2;  // ncclUint32 : ncclInt32
+    case OMPRT_U32: return 3;
+    case OMPRT_I64: return add ? 5 : 4;  // ncclUint64 : ncclInt64
+    case OMPRT_U64: return 5;
+    case OMPRT_F32: return 7;
+    case OMPRT_F64: return 8;
+    default: return -1;
+  }
+}
+}  // namespace
+
+int omprt_allreduce(void *d_buf, int64_t count, int dtype, int op, void *nccl_comm,
+                    void *stream) {
+  if (count < 0 || (count > 0 && !d_buf) || !nccl_comm)
+    return fail(OMPRT_EINVAL, "allreduce: bad arguments");
+  const int nt = nccl_dtype(dtype, op);
+  if (nt < 0) return fail(OMPRT_EINVAL, "allreduce: unknown dtype %d", dtype);
+  const int nop = op == OMPRT_OP_ADD ? 0 : (op == OMPRT_OP_MAX ? 2 : (op == OMPRT_OP_MIN ? 3 : -1));
+  if (nop < 0) return fail(OMPRT_EINVAL, "allreduce: unknown op %d", op);
+  {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (!g_nccl_allreduce) {
+      void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+      if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+      if (!h) return fail(OMPRT_EUNAVAILABLE, "allreduce: libnccl.so.2 not found (%s)", dlerror());
+      g_nccl_allreduce = reinterpret_cast<nccl_allreduce_fn>(dlsym(h, "ncclAllReduce"));
+      if (!g_nccl_allreduce) return fail(OMPRT_EUNAVAILABLE, "allreduce: no ncclAllReduce");
+    }
+  }
+  if (count == 0) return OMPRT_OK;
+  const int r = g_nccl_allreduce(d_buf, d_buf, (size_t)count, nt, nop, nccl_comm, S(stream));
+  if (r != 0) return fail(OMPRT_ECUDA, "ncclAllReduce failed (ncclResult %d)", r);
   return OMPRT_OK;
 }
 

@@ -88,6 +88,15 @@ def test_argument_validation_without_gpu():
     assert L.omprt_reduce_workspace_bytes(296, 1024, 1) >= 296 * 1024 * 8
 
 
+def test_allreduce_argument_checks():
+    # validated before NCCL is ever loaded (no GPU needed)
+    L = _lib.load()
+    assert L.omprt_allreduce(None, 1, 2, 0, C.c_void_p(1), None) == _lib.EINVAL  # null buffer
+    assert L.omprt_allreduce(C.c_void_p(1), 1, 9, 0, C.c_void_p(1), None) == _lib.EINVAL  # dtype
+    assert L.omprt_allreduce(C.c_void_p(1), 1, 2, 7, C.c_void_p(1), None) == _lib.EINVAL  # op
+    assert L.omprt_allreduce(C.c_void_p(1), 1, 2, 0, None, None) == _lib.EINVAL  # no comm
+
+
 def test_workspace_layout_covers_split_teams_and_ordered_flags():
     # SPMD launches may split a few teams over up to SMs CTAs: the team
     # partial slots (2 per CTA, 8 bytes) never shrink below 256 CTAs; ORDERED

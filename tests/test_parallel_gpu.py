@@ -88,3 +88,33 @@ def test_sharded_reduce_and_dot_two_ranks_one_gpu(cuda):
     # the deterministic (rank-ordered) combines leave identical bits on every rank
     assert got[0]["f64_sum"] == got[1]["f64_sum"]
     assert got[0]["dot"] == got[1]["dot"]
+
+
+def test_c_abi_allreduce_over_a_one_rank_nccl_comm(cuda):
+    # omprt_allreduce (the C-ABI combine of per-GPU partials) through a real
+    # NCCL communicator: one rank on cuda:0, so the all-reduce is the
+    # identity — exercises the dlopen'd ncclAllReduce, dtype/op mapping and
+    # stream ordering; the 8-rank reduction is the bench's
+    import ctypes as C
+
+    from paper_2106_03219_b200 import _lib, runtime
+
+    nccl = C.CDLL("libnccl.so.2")
+    comm = C.c_void_p()
+    devs = (C.c_int * 1)(0)
+    assert nccl.ncclCommInitAll(C.byref(comm), 1, devs) == 0
+    try:
+        L = _lib.load()
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for dt, vals, op in (("i64", [5, -7, 2**62, -(2**63)], 0), ("f64", [1.5, -2.25, 3.0], 0),
+                             ("u32", [1, 2**32 - 1], 1), ("i32", [-3, 9], 2)):
+            t = torch.tensor(vals, dtype=runtime.torch_dtype(runtime.dtype_code(dt)), device=cuda)
+            before = t.clone()
+            rc = L.omprt_allreduce(C.c_void_p(t.data_ptr()), t.numel(), runtime.dtype_code(dt),
+                                   op, comm, stream)
+            assert rc == 0, _lib.last_error()
+            torch.cuda.synchronize()
+            assert torch.equal(t.view(torch.uint8), before.view(torch.uint8)), dt
+        assert L.omprt_allreduce(C.c_void_p(1), 0, 2, 0, comm, stream) == 0  # empty
+    finally:
+        nccl.ncclCommDestroy(comm)
