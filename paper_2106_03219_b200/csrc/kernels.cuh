@@ -382,6 +382,52 @@ OMPRT_D T fold_row_in_order(const T *__restrict__ x, int64_t lo, int64_t hi, T p
   return part;
 }
 
+// This thread's schedule chunks as [lo, hi] runs, in order (block schedules:
+// one run; chunked: run_thread_chunks' sequence, loops.cuh).
+template <class F> OMPRT_D void for_each_thread_run(const LoopArgs &la, F &&f) {
+  const Bounds bd = schedule_init(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x,
+                                  threadIdx.x, blockDim.x);
+  if (la.sched != OMPRT_SCHED_STATIC_CHUNKED && la.sched != OMPRT_SCHED_DISTRIBUTE_CHUNKED) {
+    if (bd.lower <= bd.upper) f(bd.lower, bd.upper);
+    return;
+  }
+  for (int64_t lo = bd.lower; lo <= bd.limit; lo += bd.stride) {
+    int64_t hi = lo + la.chunk - 1;
+    if (hi > bd.limit) hi = bd.limit;
+    f(lo, hi);
+  }
+}
+
+// In-order y = a*x + y over [lo..hi] with max/min folded in iteration order:
+// 16-byte loads (x non-coherent, y coherent: this kernel writes it) and
+// 16-byte stores.
+OMPRT_D void axpy_run_in_order(float a, const float *__restrict__ x, float *__restrict__ y,
+                               int64_t lo, int64_t hi, float &mx, float &mn) {
+  auto one = [&](int64_t i) {
+    const float v = __fmaf_rn(a, x[i], y[i]);
+    y[i] = v;
+    mx = Red<OMPRT_OP_MAX, float>::apply(mx, v);
+    mn = Red<OMPRT_OP_MIN, float>::apply(mn, v);
+  };
+  int64_t i = lo;
+  if (((((uintptr_t)x) ^ ((uintptr_t)y)) & 15u) == 0) {
+    for (; i <= hi && (((uintptr_t)(x + i)) & 15u) != 0; ++i) one(i);
+    for (; i + 3 <= hi; i += 4) {
+      float xv[4], yv[4];
+      unpack<float>(ld_stream_v4(x + i), xv);
+      unpack<float>(ld_rw_v4(y + i), yv);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        yv[k] = __fmaf_rn(a, xv[k], yv[k]);
+        mx = Red<OMPRT_OP_MAX, float>::apply(mx, yv[k]);
+        mn = Red<OMPRT_OP_MIN, float>::apply(mn, yv[k]);
+      }
+      st_stream_v4(y + i, pack<float>(yv));
+    }
+  }
+  for (; i <= hi; ++i) one(i);
+}
+
 constexpr int kFoldBuf = 2048;  // elements of the static fold buffer
 
 template <class T, int OP>
@@ -482,12 +528,8 @@ __global__ void __launch_bounds__(kMaxThreads)
                           LoopArgs la, Workspace ws, float *out_max, float *out_min) {
   trace_begin();
   float mx = Limits<float>::lowest(), mn = Limits<float>::highest();
-  run_thread_chunks(la.sched, la.lb, la.ub, la.chunk, [&](int64_t i) {
-    const float v = __fmaf_rn(a, x[i], y[i]);
-    y[i] = v;
-    mx = Red<OMPRT_OP_MAX, float>::apply(mx, v);
-    mn = Red<OMPRT_OP_MIN, float>::apply(mn, v);
-  });
+  for_each_thread_run(
+      la, [&](int64_t lo, int64_t hi) { axpy_run_in_order(a, x, y, lo, hi, mx, mn); });
   const int64_t n = (int64_t)gridDim.x * blockDim.x;
   float *tmax = (float *)ws.thread_partials;
   float *tmin = tmax + n;
