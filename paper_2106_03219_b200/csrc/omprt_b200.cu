@@ -611,6 +611,25 @@ int omprt_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int
   return by_dtype<ReduceF>(dtype, op, d_x, la, teams, threads, mode, w, d_out, S(stream));
 }
 
+namespace {
+int launch_axpy_spmd(float a, const float *d_x, float *d_y, LoopArgs la, int teams, int threads,
+                     Workspace w, float *d_max, float *d_min, cudaStream_t st) {
+  int rc;
+  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
+  la.split = spmd_split(teams);
+  if (bulk_ok) {
+    auto kern = threads <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
+                               : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
+    const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
+    if ((rc = set_smem(kern, smem))) return rc;
+    kern<<<teams * la.split, threads, smem, st>>>(a, d_x, d_y, la, w, d_max, d_min);
+  } else {
+    k_axpy_minmax<4><<<teams * la.split, threads, 0, st>>>(a, d_x, d_y, la, w, d_max, d_min);
+  }
+  return check_launch("omprt_axpy_minmax");
+}
+}  // namespace
+
 int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t ub, int sched,
                       int64_t chunk, int teams, int threads, int mode, void *d_ws, float *d_max,
                       float *d_min, void *stream) {
@@ -620,22 +639,27 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
     return fail(OMPRT_EINVAL, "axpy_minmax: null device pointer");
   LoopArgs la{lb, ub, chunk, sched};
   Workspace w = ws_carve(d_ws, teams, 2);
-  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
-  if (mode == OMPRT_MODE_ORDERED) {
+  if (mode != OMPRT_MODE_ORDERED)
+    return launch_axpy_spmd(a, d_x, d_y, la, teams, threads, w, d_max, d_min, S(stream));
+  if (g_variant == kOrderedLiteral || !ord_rows_ok(la, d_y)) {
     k_axpy_minmax_ordered<<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
-  } else if (bulk_ok) {
-    la.split = spmd_split(teams);
-    auto kern = threads <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
-                               : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
-    const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
-    if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams * la.split, threads, smem, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
-  } else {
-    la.split = spmd_split(teams);
-    k_axpy_minmax<4><<<teams * la.split, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max,
-                                                                   d_min);
+    return check_launch("omprt_axpy_minmax(ordered)");
   }
-  return check_launch("omprt_axpy_minmax");
+  // ORDERED: y = a*x + y is elementwise, so the SPMD kernel writes the same
+  // y (its own max/min go to a scratch pair in the workspace header and are
+  // dropped); then max and min are folded over the new y in the reference
+  // order — every OpenMP thread its chunks in order, partials in global
+  // thread order, starting from the cells — by the ORDERED reductions,
+  // exactly what the literal walk computes, at streaming speed.
+  float *scratch = reinterpret_cast<float *>(static_cast<unsigned char *>(d_ws) + 128);
+  if ((rc = launch_axpy_spmd(a, d_x, d_y, la, teams, threads, w, scratch, scratch + 1,
+                             S(stream))))
+    return rc;
+  if ((rc = launch_reduce_t<float, OMPRT_OP_MAX>(d_y, la, teams, threads, OMPRT_MODE_ORDERED, w,
+                                                  d_max, S(stream))))
+    return rc;
+  return launch_reduce_t<float, OMPRT_OP_MIN>(d_y, la, teams, threads, OMPRT_MODE_ORDERED, w,
+                                              d_min, S(stream));
 }
 
 int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int sched,
