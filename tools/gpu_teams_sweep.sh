@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+: > gpurun_out/teams_sweep.txt
+for t in 148 136 128 120 112 148; do
+  timeout 300 python bench.py --teams $t --steps 1000 --warmup 10 --e2e-steps 0 --no-cpu-baseline --ordered-steps 0 > gpurun_out/bench_T$t.log 2>&1
+  grep '^{' gpurun_out/bench_T$t.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($t, d['value'], d['roofline']['achieved'], d['clocks']['sm_mhz'], d['clocks']['reasons'])" >> gpurun_out/teams_sweep.txt
+done
