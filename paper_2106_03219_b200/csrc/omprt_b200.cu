@@ -655,11 +655,25 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
   if ((rc = launch_axpy_spmd(a, d_x, d_y, la, teams, threads, w, scratch, scratch + 1,
                              S(stream))))
     return rc;
-  if ((rc = launch_reduce_t<float, OMPRT_OP_MAX>(d_y, la, teams, threads, OMPRT_MODE_ORDERED, w,
-                                                  d_max, S(stream))))
-    return rc;
-  return launch_reduce_t<float, OMPRT_OP_MIN>(d_y, la, teams, threads, OMPRT_MODE_ORDERED, w,
-                                              d_min, S(stream));
+  // one pass folding max and min together (float2 partials, two chains)
+  const int nw = ord_default_nw(teams, threads);
+  const int s512 = OrdSmem<float, 128, 1>::stages_for(nw);
+  const int s256 = OrdSmem<float, 64, 1>::stages_for(nw);
+  const int grid = ord_grid(teams, threads, nw);
+  if (s512 >= 3) {
+    const size_t ring = (size_t)nw * OrdSmem<float, 128, 1>::warp_bytes(s512);
+    if ((rc = set_smem(k_minmax_ordered_rows<128>, ring + kFolderSmem))) return rc;
+    k_minmax_ordered_rows<128><<<grid, (nw + 1) * 32, ring + kFolderSmem, S(stream)>>>(
+        d_y, la, teams, threads, w, d_max, d_min, s512, next_epoch(), (uint32_t)ring,
+        ord_segments(la, teams, threads, 128));
+  } else {
+    const size_t ring = (size_t)nw * OrdSmem<float, 64, 1>::warp_bytes(s256);
+    if ((rc = set_smem(k_minmax_ordered_rows<64>, ring + kFolderSmem))) return rc;
+    k_minmax_ordered_rows<64><<<grid, (nw + 1) * 32, ring + kFolderSmem, S(stream)>>>(
+        d_y, la, teams, threads, w, d_max, d_min, s256, next_epoch(), (uint32_t)ring,
+        ord_segments(la, teams, threads, 64));
+  }
+  return check_launch("omprt_axpy_minmax(ordered max/min)");
 }
 
 int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int sched,

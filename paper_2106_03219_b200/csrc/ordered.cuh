@@ -427,13 +427,12 @@ OMPRT_D void ord_folder_load(const T *tp, int64_t P, const uint64_t *flags, uint
   for (int k = 0; k < N; ++k) L.v[k] = (first + k < P) ? ld_cg(tp + first + k) : T();
 }
 
-template <int OP, class T, class Combine>
-OMPRT_D void ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epoch, T *out,
-                        T *ring, Combine &&comb) {
+template <class T, class Combine>
+OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epoch, T acc,
+                     T *ring, Combine &&comb) {
   constexpr int N = FoldLoad<T>::N;
   const uint32_t lane = threadIdx.x & 31u;
   const int64_t nb = (P + kFoldPer - 1) / kFoldPer;
-  T acc = *out;
   FoldLoad<T> L;
   ord_folder_load<T>(tp, P, flags, epoch, 0, L);
 #pragma unroll
@@ -457,10 +456,9 @@ OMPRT_D void ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t 
     }
     __syncwarp();
   }
-  if (lane == 0) {
-    *out = acc;
+  if (lane == 0)
     trace_record(gridDim.x * ((blockDim.x >> 5) - 1), kTraceFolder, (uint32_t)nb, trace_t0());
-  }
+  return acc;  // the same in every lane
 }
 
 template <int OP, class T> struct RedComb {
@@ -488,9 +486,11 @@ __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
   uint64_t *flags = (uint64_t *)(ws.thread_partials + ord_flags_offset(P));
   if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
     extern __shared__ __align__(16) unsigned char ord_smem[];
-    if (blockIdx.x == 0)
-      ord_folder<OP, T>(tp, P, flags, epoch + (uint64_t)seg, out, (T *)(ord_smem + ring_off),
-                        RedComb<OP, T>());
+    if (blockIdx.x == 0) {
+      const T v = ord_folder<T>(tp, P, flags, epoch + (uint64_t)seg, *out,
+                                (T *)(ord_smem + ring_off), RedComb<OP, T>());
+      if ((threadIdx.x & 31u) == 0) *out = v;
+    }
     return;
   }
   OrdReduceFold<T, OP, W> f{Red<OP, T>::identity(), tp};
@@ -510,15 +510,91 @@ __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
   uint64_t *flags = (uint64_t *)(ws.thread_partials + ord_flags_offset(P));
   if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
     extern __shared__ __align__(16) unsigned char ord_smem[];
-    if (blockIdx.x == 0)
-      ord_folder<OMPRT_OP_ADD, double>(tp, P, flags, epoch + (uint64_t)seg, out,
-                                       (double *)(ord_smem + ring_off),
-                                       RedComb<OMPRT_OP_ADD, double>());
+    if (blockIdx.x == 0) {
+      const double v = ord_folder<double>(tp, P, flags, epoch + (uint64_t)seg, *out,
+                                          (double *)(ord_smem + ring_off),
+                                          RedComb<OMPRT_OP_ADD, double>());
+      if ((threadIdx.x & 31u) == 0) *out = v;
+    }
     return;
   }
   OrdDotFold<W> f{0.0, tp};
   const double *src[2] = {x, y};
   ord_groups<double, W, 2>(la, teams, threads, src, stages, f, flags, epoch, seg, ws.ticket);
+}
+
+// max and min folded together in one ORDERED pass (axpy's ORDERED mode):
+// the per-thread partials are float2 {max, min}, the folder carries both
+// chains (independent, so interleaved at the latency of one).
+template <int W> struct OrdMinMaxFold {
+  static constexpr int V = 4;
+  float mx, mn;
+  float2 *tp;
+  OMPRT_D void operator()(const float *const (&rows)[1], int s, int e) {
+    const float *r = rows[0];
+    if (s == 0 && e == W - 1) {
+#pragma unroll 4
+      for (int q = 0; q < W / V; ++q) {
+        float v[V];
+        lds_vec<float, V>(v, r + q * V);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          mx = Red<OMPRT_OP_MAX, float>::apply(mx, v[k]);
+          mn = Red<OMPRT_OP_MIN, float>::apply(mn, v[k]);
+        }
+      }
+    } else {
+      for (int o = s; o <= e; ++o) {
+        mx = Red<OMPRT_OP_MAX, float>::apply(mx, r[o]);
+        mn = Red<OMPRT_OP_MIN, float>::apply(mn, r[o]);
+      }
+    }
+  }
+  OMPRT_D void publish(int64_t g) {
+    tp[g] = make_float2(mx, mn);
+    mx = Limits<float>::lowest();
+    mn = Limits<float>::highest();
+  }
+  OMPRT_D void resume(int64_t g) {
+    const float2 v = ld_cg(tp + g);
+    mx = v.x;
+    mn = v.y;
+  }
+};
+
+struct MinMaxComb {
+  OMPRT_D float2 operator()(float2 a, float2 b) const {
+    return make_float2(Red<OMPRT_OP_MAX, float>::apply(a.x, b.x),
+                       Red<OMPRT_OP_MIN, float>::apply(a.y, b.y));
+  }
+};
+
+template <int W>
+__global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
+    k_minmax_ordered_rows(const float *__restrict__ y, LoopArgs la, int teams, int threads,
+                          Workspace ws, float *out_max, float *out_min, int stages,
+                          uint64_t epoch, uint32_t ring_off, int seg) {
+  trace_begin();
+  __syncthreads();
+  const int64_t P = (int64_t)teams * threads;
+  float2 *tp = (float2 *)ws.thread_partials;
+  uint64_t *flags = (uint64_t *)(ws.thread_partials + ord_flags_offset(P));
+  if ((threadIdx.x >> 5) == (blockDim.x >> 5) - 1) {
+    extern __shared__ __align__(16) unsigned char ord_smem[];
+    if (blockIdx.x == 0) {
+      const float2 v = ord_folder<float2>(tp, P, flags, epoch + (uint64_t)seg,
+                                          make_float2(*out_max, *out_min),
+                                          (float2 *)(ord_smem + ring_off), MinMaxComb());
+      if ((threadIdx.x & 31u) == 0) {
+        *out_max = v.x;
+        *out_min = v.y;
+      }
+    }
+    return;
+  }
+  OrdMinMaxFold<W> f{Limits<float>::lowest(), Limits<float>::highest(), tp};
+  const float *src[1] = {y};
+  ord_groups<float, W, 1>(la, teams, threads, src, stages, f, flags, epoch, seg, ws.ticket);
 }
 
 // Host side: can the row-group kernels take this launch?  x (and y) must be
