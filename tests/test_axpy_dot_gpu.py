@@ -96,3 +96,30 @@ def test_dot_full_shard(cuda):
     assert abs(got - truth) <= 1e-6 * truth
     del x, y
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n,teams,threads,sched", [(1 << 20, 8, 64, "distribute"),
+                                                   (1 << 24, 8, 64, "static"),
+                                                   (300_001, 5, 96, "static_chunked")])
+def test_axpy_ordered_keeps_the_reference_order_of_signed_zeros(cuda, n, teams, threads, sched):
+    # max/min are exact but not order-free for +0/-0 (a < b is false both
+    # ways): the ORDERED result's zero sign must be the reference order's
+    chunk = 64
+    for base in (-1.0, 1.0):  # max picks among zeros, then min does
+        x = np.zeros(n, dtype=np.float32)
+        y = np.full(n, base, dtype=np.float32)
+        i = np.arange(n)
+        neg = (i % 997) == 5
+        pos = (i % 1009) == 3
+        x[neg], y[neg] = np.float32(-0.0), np.float32(-0.0)  # 1*-0 + -0 = -0
+        x[pos], y[pos] = np.float32(0.0), np.float32(0.0)    # 1*+0 + +0 = +0
+        yo = y.copy()
+        mx, mn = O.axpy_minmax(1.0, x, yo, 0, n - 1, SCHEDS[sched], chunk, teams, threads,
+                               -np.inf, np.inf)
+        xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+        gmx, gmn = runtime.axpy_minmax(1.0, xd, yd, sched=sched, chunk=chunk, teams=teams,
+                                       threads=threads, mode="ordered")
+        got = np.array([gmx.item(), gmn.item()], dtype=np.float32)
+        want = np.array([mx, mn], dtype=np.float32)
+        assert got.tobytes() == want.tobytes(), (base, sched, got, want)
+        assert np.array_equal(yd.cpu().numpy().view(np.uint32), yo.view(np.uint32))
