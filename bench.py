@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--ordered-steps", type=int, default=50,
                    help="steps of the ORDERED-mode (reference-order, bit-identical) leg")
     p.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU")
+    p.add_argument("--exchange", choices=["nccl", "p2p"], default="nccl",
+                   help="N > 1: combine the per-GPU partials with NCCL (overlapped with the "
+                        "next step) or inside the reduction kernel over NVLink peer memory")
     p.add_argument("--no-overlap", action="store_true",
                    help="N > 1: run each step's all-reduce on the compute stream (no overlap)")
     p.add_argument("--backend", default="nccl",
@@ -236,7 +239,9 @@ def run_ours(args) -> None:
     # into the cell) runs on a side stream, overlapping step k+1's shard
     # reduction (double-buffered partials; the NCCL kernel fits beside the
     # one-CTA-per-SM reduce kernel)
-    comm = torch.cuda.Stream(dev) if (G > 1 and not args.no_overlap) else None
+    px = parallel.PeerExchange(dev) if (G > 1 and args.exchange == "p2p") else None
+    comm = (torch.cuda.Stream(dev) if (G > 1 and px is None and not args.no_overlap)
+            else None)
     partials = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
     freed = [torch.cuda.Event(), torch.cuda.Event()]
     nstep = [0]
@@ -245,6 +250,11 @@ def run_ours(args) -> None:
         if G == 1:
             # the whole hot path on one GPU: one construct launch into the cell
             runtime.reduce(x, "add", sched=args.sched, teams=teams, threads=threads, out=out)
+            return
+        if px is not None:
+            # one kernel: shard reduction + the peer-memory exchange + the
+            # rank-ordered fold into the cell
+            px.reduce(x, "add", out=out, sched=args.sched, teams=teams, threads=threads)
             return
         if comm is None:
             partial.zero_()
@@ -451,9 +461,12 @@ def run_ours(args) -> None:
             "config": {"workload": "C2 teams distribute parallel for fp64 sum reduction, SPMD",
                        "n_per_gpu": n, "n_global": G * n, "schedule": args.sched,
                        "teams": teams, "threads": threads, "mode": "spmd",
-                       "parallelism": f"dp{G} (static_bounds shards + {args.backend.upper()} all-reduce"
-                                      + (", overlapped with the next step's shard)" if comm is not None
-                                         else ")"),
+                       "parallelism": (f"dp{G} (static_bounds shards + partials exchanged inside "
+                                       "the reduction kernel over NVLink peer memory)"
+                                       if px is not None else
+                                       f"dp{G} (static_bounds shards + {args.backend.upper()} "
+                                       "all-reduce" + (", overlapped with the next step's shard)"
+                                                       if comm is not None else ")")),
                        "l2": "input 8 GiB per GPU >> 126 MB L2; no flush needed",
                        "frac_of_hbm_peak": round(gbs / G / pk["hbm_gbs"], 4),
                        "frac_of_nominal_8tbs": round(gbs / G / 8000.0, 4)},
@@ -472,11 +485,13 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "ordered": ordered,
-            "gpu_launches": args.steps * (1 if G == 1 else 2),  # reduce (+ combine) per step
+            "gpu_launches": args.steps * (1 if (G == 1 or px is not None) else 2),
             "clocks": clocks,
             "parity": parity,
         }
         print(json.dumps(line), flush=True)
+    if px is not None:
+        px.close()
     if G > 1:
         dist.barrier()
         dist.destroy_process_group()

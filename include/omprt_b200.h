@@ -155,6 +155,27 @@ int omprt_set_variant(int variant);
 int omprt_allreduce(void *d_buf, int64_t count, int dtype, int op, void *nccl_comm,
                     void *stream);
 
+/* Fused multi-GPU combine (the all-reduce inside the reduction kernel):
+ * each rank creates a mailbox (two banks x world slots of 16 bytes, zeroed)
+ * and exports it as a CUDA IPC handle (omprt_ipc_handle_bytes() bytes); the
+ * ranks exchange handles out of band and open each other's mailboxes; a
+ * device array of the world's mailbox pointers (rank order, own included)
+ * is passed to omprt_reduce_exchange.  Its last team stores this GPU's
+ * partial into every rank's slot over NVLink peer memory and folds the
+ * world's partials in rank order into d_out — one kernel, identical bits on
+ * every rank.  `key` (nonzero, the same on all ranks) must differ at every
+ * call; `step` selects the bank (calls on one mailbox alternate).  A peer
+ * that does not arrive within 20 s raises OMPRT_TRAP_DEADLOCK. */
+size_t omprt_ipc_handle_bytes(void);
+int omprt_mailbox_create(int world, void **d_mailbox, void *ipc_handle);
+int omprt_mailbox_open(const void *ipc_handle, void **d_ptr);
+int omprt_mailbox_close(void *d_ptr);
+int omprt_mailbox_destroy(void *d_mailbox);
+int omprt_reduce_exchange(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int sched,
+                          int64_t chunk, int teams, int threads, void *d_ws, void *d_out,
+                          const void *d_peers, int rank, int world, uint64_t key, uint64_t step,
+                          void *stream);
+
 /* Per-team trace ring — the B200 analog of the vgpu's collect_trace
  * (vgpu.py:351-353, tgt_target(collect_trace=True) host.py:255-296).  While a
  * device buffer of `capacity` 32-byte records is installed, every construct

@@ -59,6 +59,14 @@ _SIGS = {
     "omprt_set_unroll": ([C.c_int], C.c_int),
     "omprt_set_variant": ([C.c_int], C.c_int),
     "omprt_set_trace": ([C.c_void_p, C.c_int64], C.c_int),
+    "omprt_ipc_handle_bytes": ([], C.c_size_t),
+    "omprt_mailbox_create": ([C.c_int, C.POINTER(C.c_void_p), C.c_void_p], C.c_int),
+    "omprt_mailbox_open": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+    "omprt_mailbox_close": ([C.c_void_p], C.c_int),
+    "omprt_mailbox_destroy": ([C.c_void_p], C.c_int),
+    "omprt_reduce_exchange": ([C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int,
+                               C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p], C.c_int),
     "omprt_allreduce": ([C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p],
                         C.c_int),
     "omprt_num_sms": ([], C.c_int),

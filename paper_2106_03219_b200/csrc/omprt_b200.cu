@@ -16,6 +16,7 @@
 #include "bulk.cuh"
 #include "generic.cuh"
 #include "ordered.cuh"
+#include "exchange.cuh"
 
 using namespace omprt;
 
@@ -334,6 +335,33 @@ template <class T> struct ReduceF {
   }
 };
 
+template <class T, int OP>
+int launch_exchange_t(const void *x, LoopArgs la, int teams, int threads, Workspace w, void *out,
+                      const Exchange &xc, cudaStream_t st) {
+  auto kern = k_reduce_bulk_exchange<T, OP, kBulkStages, kBulkStageBytes>;
+  const size_t smem = BulkSmem<kBulkStages, kBulkStageBytes>::bytes;
+  int rc = set_smem(kern, smem);
+  if (rc) return rc;
+  la.split = spmd_split(teams);
+  kern<<<teams * la.split, threads, smem, st>>>((const T *)x, la, w, (T *)out, xc);
+  return check_launch("omprt_reduce_exchange");
+}
+
+template <class T> struct ExchangeF {
+  static int run(int op, const void *x, LoopArgs la, int teams, int threads, Workspace w,
+                 void *out, Exchange xc, cudaStream_t st) {
+    switch (op) {
+      case OMPRT_OP_ADD:
+        return launch_exchange_t<T, OMPRT_OP_ADD>(x, la, teams, threads, w, out, xc, st);
+      case OMPRT_OP_MAX:
+        return launch_exchange_t<T, OMPRT_OP_MAX>(x, la, teams, threads, w, out, xc, st);
+      case OMPRT_OP_MIN:
+        return launch_exchange_t<T, OMPRT_OP_MIN>(x, la, teams, threads, w, out, xc, st);
+    }
+    return fail(OMPRT_EINVAL, "unknown op %d", op);
+  }
+};
+
 template <class T> struct FillF {
   static int run(void *x, int64_t n, uint64_t seed, int k, int64_t offset, cudaStream_t st) {
     if (n <= 0) return OMPRT_OK;
@@ -523,6 +551,71 @@ int omprt_allreduce(void *d_buf, int64_t count, int dtype, int op, void *nccl_co
   const int r = g_nccl_allreduce(d_buf, d_buf, (size_t)count, nt, nop, nccl_comm, S(stream));
   if (r != 0) return fail(OMPRT_ECUDA, "ncclAllReduce failed (ncclResult %d)", r);
   return OMPRT_OK;
+}
+
+// ------------------------------------------- fused multi-GPU exchange (IPC)
+
+size_t omprt_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int omprt_mailbox_create(int world, void **d_mailbox, void *ipc_handle) {
+  if (world < 1 || !d_mailbox || !ipc_handle)
+    return fail(OMPRT_EINVAL, "mailbox_create: bad arguments");
+  const size_t bytes = (size_t)2 * world * 16;  // two banks x world slots {value, key}
+  void *p = nullptr;
+  OMPRT_CUDA(cudaMalloc(&p, bytes));
+  OMPRT_CUDA(cudaMemset(p, 0, bytes));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(OMPRT_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  }
+  std::memcpy(ipc_handle, &h, sizeof(h));
+  *d_mailbox = p;
+  return OMPRT_OK;
+}
+
+int omprt_mailbox_open(const void *ipc_handle, void **d_ptr) {
+  if (!ipc_handle || !d_ptr) return fail(OMPRT_EINVAL, "mailbox_open: bad arguments");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, ipc_handle, sizeof(h));
+  OMPRT_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return OMPRT_OK;
+}
+
+int omprt_mailbox_close(void *d_ptr) {
+  if (!d_ptr) return fail(OMPRT_EINVAL, "mailbox_close: null");
+  OMPRT_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return OMPRT_OK;
+}
+
+int omprt_mailbox_destroy(void *d_mailbox) {
+  if (!d_mailbox) return fail(OMPRT_EINVAL, "mailbox_destroy: null");
+  OMPRT_CUDA(cudaFree(d_mailbox));
+  return OMPRT_OK;
+}
+
+int omprt_reduce_exchange(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int sched,
+                          int64_t chunk, int teams, int threads, void *d_ws, void *d_out,
+                          const void *d_peers, int rank, int world, uint64_t key, uint64_t step,
+                          void *stream) {
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  if (!d_ws || !d_out || !d_peers || (!d_x && ub >= lb) || world < 1 || rank < 0 ||
+      rank >= world || key == 0)
+    return fail(OMPRT_EINVAL, "reduce_exchange: bad arguments");
+  if (threads < 64 || threads % 32 != 0)
+    return fail(OMPRT_EINVAL, "reduce_exchange: threads must be a multiple of 32, >= 64");
+  LoopArgs la{lb, ub, chunk, sched};
+  Workspace w = ws_carve(d_ws, teams, 2);
+  Exchange xc;
+  xc.peers = reinterpret_cast<uint64_t *const *>(const_cast<void *>(d_peers));
+  xc.rank = rank;
+  xc.world = world;
+  xc.key = key;
+  xc.bank = (uint32_t)(step & 1);
+  xc.timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s: a missing peer traps (Deadlock)
+  return by_dtype<ExchangeF>(dtype, op, d_x, la, teams, threads, w, d_out, xc, S(stream));
 }
 
 int omprt_set_trace(void *d_records, int64_t capacity) {

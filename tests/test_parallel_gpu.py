@@ -118,3 +118,59 @@ def test_c_abi_allreduce_over_a_one_rank_nccl_comm(cuda):
         assert L.omprt_allreduce(C.c_void_p(1), 0, 2, 0, comm, stream) == 0  # empty
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+def _xchg_worker(rank: int, world: int, port: int, q) -> None:
+    from paper_2106_03219_b200 import parallel, runtime
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        n = 2_000_003
+        lo, hi = parallel.shard(0, n - 1, rank, world)
+        xi = runtime.synthetic(hi - lo + 1, "i64", O.SEED, 0, offset=lo, device=dev)
+        xf = runtime.synthetic(hi - lo + 1, "f64", O.SEED, 0, offset=lo, device=dev)
+        px = parallel.PeerExchange(dev)
+        res = {"i64": [], "f64": [], "max": []}
+        for _ in range(5):  # several steps: the mailbox banks alternate
+            out = torch.zeros(1, dtype=torch.int64, device=dev)
+            px.reduce(xi, "add", out=out, teams=16, threads=128)
+            res["i64"].append(int(out.item()))
+            of = torch.zeros(1, dtype=torch.float64, device=dev)
+            px.reduce(xf, "add", out=of, sched="distribute", teams=8, threads=256)
+            res["f64"].append(float(of.item()))
+            om = torch.full((1,), np.iinfo(np.int64).min, dtype=torch.int64, device=dev)
+            px.reduce(xi, "max", out=om, teams=4, threads=64)
+            res["max"].append(int(om.item()))
+        px.close()
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_peer_exchange_two_ranks_one_gpu(cuda):
+    # omprt_reduce_exchange: the combine inside the reduction kernel through
+    # CUDA IPC mailboxes (two processes on one GPU map each other's buffers)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xchg_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = 2_000_003
+    want = int(O.reduce_flat_gen(0, n - 1, O.I64, O.ADD))
+    want_max = int(O.reduce_flat_gen(0, n - 1, O.I64, O.MAX, init=np.iinfo(np.int64).min))
+    exact = O.exact_sum_gen(0, n - 1, O.F64)
+    for r in range(world):
+        assert got[r]["i64"] == [want] * 5
+        assert got[r]["max"] == [want_max] * 5
+        assert all(abs(v - exact) <= 1e-6 * exact for v in got[r]["f64"])
+    assert got[0]["f64"] == got[1]["f64"]  # rank-ordered fold: the same bits everywhere

@@ -1,5 +1,4 @@
 set -x
 mkdir -p gpurun_out
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 50 --warmup 3 --e2e-steps 1 --backend gloo > gpurun_out/tr2_gloo.log 2>&1
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --steps 50 --warmup 3 --e2e-steps 1 --backend gloo --no-overlap > gpurun_out/tr2_gloo_noov.log 2>&1
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 200 --warmup 5 --e2e-steps 1 > gpurun_out/tr1.log 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29514 bench.py --gpus 2 --steps 50 --warmup 3 --e2e-steps 1 --backend gloo --exchange p2p > gpurun_out/tr2_p2p.log 2>&1
