@@ -174,3 +174,36 @@ def test_fused_peer_exchange_two_ranks_one_gpu(cuda):
         assert got[r]["max"] == [want_max] * 5
         assert all(abs(v - exact) <= 1e-6 * exact for v in got[r]["f64"])
     assert got[0]["f64"] == got[1]["f64"]  # rank-ordered fold: the same bits everywhere
+
+
+def test_reduce_exchange_single_rank_matches_reduce(cuda):
+    # omprt_reduce_exchange with a world of one (the mailbox is the rank's
+    # own): the exchange epilogue folds the lone GPU partial into the cell,
+    # so the result equals the plain construct's, for every key/bank
+    import ctypes as C
+
+    from paper_2106_03219_b200 import _lib, runtime
+
+    L = _lib.load()
+    hb = L.omprt_ipc_handle_bytes()
+    handle = (C.c_char * hb)()
+    mb = C.c_void_p()
+    assert L.omprt_mailbox_create(1, C.byref(mb), handle) == 0
+    try:
+        peers = torch.tensor([mb.value], dtype=torch.int64, device=cuda)
+        x = runtime.synthetic(5_000_011, "i64", O.SEED, 3, device=cuda)
+        want = int(runtime.reduce(x, "add", teams=148, threads=256).item())
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ws = runtime.reduce_workspace(cuda, 148, 256, 0)
+        for step in range(4):
+            out = torch.zeros(1, dtype=torch.int64, device=cuda)
+            rc = L.omprt_reduce_exchange(C.c_void_p(x.data_ptr()), 0, x.numel() - 1,
+                                         runtime.dtype_code("i64"), 0, 0, 1, 148, 256,
+                                         C.c_void_p(ws.data_ptr()), C.c_void_p(out.data_ptr()),
+                                         C.c_void_p(peers.data_ptr()), 0, 1, 1000 + step, step,
+                                         stream)
+            assert rc == 0, _lib.last_error()
+            assert int(out.item()) == want
+        assert runtime.check_trap(cuda) is None
+    finally:
+        L.omprt_mailbox_destroy(mb)
