@@ -30,6 +30,25 @@ runtime.set_variant(0)
 # few-team SPMD launches split over CTAs (team_set_cta)
 runtime.reduce(xi, sched="static", teams=1, threads=128)
 runtime.reduce(x, sched="static_chunked", chunk=5, teams=3, threads=64)
+# the fused exchange epilogue with a world of one (own mailbox)
+import ctypes as C  # noqa: E402
+L = _lib.load()
+_h = (C.c_char * L.omprt_ipc_handle_bytes())()
+_mb = C.c_void_p()
+L.omprt_mailbox_create(1, C.byref(_mb), _h)
+_peers = torch.tensor([_mb.value], dtype=torch.int64, device=dev)
+_ws = runtime.reduce_workspace(dev, 8, 256, 0)
+_out = torch.zeros(1, dtype=torch.float64, device=dev)
+for _k in range(2):
+    L.omprt_reduce_exchange(C.c_void_p(x.data_ptr()), 0, x.numel() - 1, 5, 0, 2, 1, 8, 256,
+                            C.c_void_p(_ws.data_ptr()), C.c_void_p(_out.data_ptr()),
+                            C.c_void_p(_peers.data_ptr()), 0, 1, 77 + _k, _k,
+                            C.c_void_p(torch.cuda.current_stream().cuda_stream))
+torch.cuda.synchronize()
+L.omprt_mailbox_destroy(_mb)
+# trace ring installed around a construct
+with runtime.Trace(dev):
+    runtime.reduce(x, teams=8, threads=256)
 runtime.set_unroll(8)
 runtime.reduce(x, teams=8, threads=256)
 runtime.set_unroll(4)
