@@ -178,9 +178,11 @@ inline int ord_default_nw(int teams, int threads) {
 // omprt_set_variant(31) keeps the static assignment.
 constexpr int kOrderedStatic = 31;
 
-int ord_segments(const LoopArgs &la, int teams, int threads, int window_elems) {
+int ord_segments(const LoopArgs &la, int teams, int threads, int window_elems, int elem_bytes) {
   if (g_variant == kOrderedStatic) return 0;
-  if (la.sched == OMPRT_SCHED_STATIC_CHUNKED || la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED)
+  // chunked rows: segments need every chunk at the same 16-byte offset
+  if ((la.sched == OMPRT_SCHED_STATIC_CHUNKED || la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED) &&
+      la.chunk % (16 / elem_bytes) != 0)
     return 0;
   if (la.ub < la.lb) return 0;
   const int64_t P = (int64_t)teams * threads;
@@ -204,7 +206,7 @@ int launch_ordered_rows(const T *xp, LoopArgs la, int teams, int threads, int nw
   if (rc) return rc;
   kern<<<ord_grid(teams, threads, nw), (nw + 1) * 32, smem, st>>>(
       xp, la, teams, threads, w, op, stages, next_epoch(), (uint32_t)ring,
-      ord_segments(la, teams, threads, W));
+      ord_segments(la, teams, threads, W, (int)sizeof(T)));
   return check_launch("omprt_reduce(ordered rows)");
 }
 
@@ -758,13 +760,13 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
     if ((rc = set_smem(k_minmax_ordered_rows<128>, ring + kFolderSmem))) return rc;
     k_minmax_ordered_rows<128><<<grid, (nw + 1) * 32, ring + kFolderSmem, S(stream)>>>(
         d_y, la, teams, threads, w, d_max, d_min, s512, next_epoch(), (uint32_t)ring,
-        ord_segments(la, teams, threads, 128));
+        ord_segments(la, teams, threads, 128, 4));
   } else {
     const size_t ring = (size_t)nw * OrdSmem<float, 64, 1>::warp_bytes(s256);
     if ((rc = set_smem(k_minmax_ordered_rows<64>, ring + kFolderSmem))) return rc;
     k_minmax_ordered_rows<64><<<grid, (nw + 1) * 32, ring + kFolderSmem, S(stream)>>>(
         d_y, la, teams, threads, w, d_max, d_min, s256, next_epoch(), (uint32_t)ring,
-        ord_segments(la, teams, threads, 64));
+        ord_segments(la, teams, threads, 64, 4));
   }
   return check_launch("omprt_axpy_minmax(ordered max/min)");
 }
@@ -793,21 +795,21 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
         if ((rc = set_smem(k_dot_ordered_rows<64>, smem))) return rc;
         k_dot_ordered_rows<64><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
             d_x, d_y, la, teams, threads, w, d_out, s512, ep, (uint32_t)ring,
-            ord_segments(la, teams, threads, 64));
+            ord_segments(la, teams, threads, 64, 8));
       } else if (s256 >= 2) {
         const size_t ring = (size_t)nw * OrdSmem<double, 32, 2>::warp_bytes(s256);
         const size_t smem = ring + kFolderSmem;
         if ((rc = set_smem(k_dot_ordered_rows<32>, smem))) return rc;
         k_dot_ordered_rows<32><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
             d_x, d_y, la, teams, threads, w, d_out, s256, ep, (uint32_t)ring,
-            ord_segments(la, teams, threads, 32));
+            ord_segments(la, teams, threads, 32, 8));
       } else if (s128 >= 2) {
         const size_t ring = (size_t)nw * OrdSmem<double, 16, 2>::warp_bytes(s128);
         const size_t smem = ring + kFolderSmem;
         if ((rc = set_smem(k_dot_ordered_rows<16>, smem))) return rc;
         k_dot_ordered_rows<16><<<grid, (nw + 1) * 32, smem, S(stream)>>>(
             d_x, d_y, la, teams, threads, w, d_out, s128, ep, (uint32_t)ring,
-            ord_segments(la, teams, threads, 16));
+            ord_segments(la, teams, threads, 16, 8));
       } else {
         k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
       }

@@ -115,13 +115,37 @@ template <int W, int V> struct OrdRow {
     a = p & ~(int64_t)(V - 1);
   }
   OMPRT_D bool live() const { return p <= hi && left > 0; }
-  // windows of a (non-chunked) row, and positioning at window w0 with a
-  // budget of n windows: segment s of a row is windows [s*K, s*K + K)
-  OMPRT_D int64_t windows() const { return p <= hi ? (hi - a) / W + 1 : 0; }
+  // Windows of the row, and positioning at window w0 with a budget of n
+  // windows (segment s of a row is windows [s*K, s*K + K)).  Chunked rows
+  // (the host only asks when chunk and stride are multiples of V, so every
+  // chunk of the row has the same 16-byte offset `off`) have wc windows per
+  // full chunk.  Call right after init().
+  OMPRT_D int64_t windows() const {
+    if (p > hi) return 0;
+    if (!chunked) return (hi - a) / W + 1;
+    const int64_t off = p - a;
+    const int64_t nch = (limit - clo) / stride + 1;
+    const int64_t wc = (chunk + off + W - 1) / W;
+    const int64_t lo_last = clo + (nch - 1) * stride;
+    int64_t cl = limit - lo_last + 1;
+    if (cl > chunk) cl = chunk;
+    return (nch - 1) * wc + (cl + off + W - 1) / W;
+  }
   OMPRT_D void seek(int64_t w0, int64_t n) {
     if (w0 > 0) {
-      a += w0 * W;
-      p = a;
+      if (!chunked) {
+        a += w0 * W;
+        p = a;
+      } else {
+        const int64_t off = p - a;
+        const int64_t wc = (chunk + off + W - 1) / W;
+        const int64_t k = w0 / wc, j = w0 - k * wc;
+        clo += k * stride;
+        hi = clo + chunk - 1;
+        if (hi > limit) hi = limit;
+        a = clo - off + j * W;
+        p = j == 0 ? clo : a;
+      }
     }
     left = n;
   }
