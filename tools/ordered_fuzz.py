@@ -1,6 +1,8 @@
 """Randomised bit-exactness fuzz of every ORDERED path against the oracle's
 reference order: fp32/fp64 sums and max/min (row-group kernels with static
-and dynamic segments, literal walk), fp64 dot, axpy + max/min.  Sizes are
+and dynamic segments, literal walk), fp64 dot, axpy + max/min; plus SPMD
+integer reductions (bit-exact: every bulk / LDG / team-split path) and SPMD
+fp64 sums (within 1e-6 of the exact sum).  Sizes are
 chosen so that rows span many windows (dynamic segments > 1) as well as
 single windows.  Prints one JSON summary line; exits 1 on any mismatch.
 
@@ -33,7 +35,7 @@ def main():
     rng = np.random.default_rng(a.seed)
     dev = torch.device("cuda", 0)
     N = 6_000_011
-    data = {dt: O.fill(N, dt, O.SEED, 5) for dt in (O.F32, O.F64)}
+    data = {dt: O.fill(N, dt, O.SEED, 5) for dt in (O.F32, O.F64, O.I64, O.U32)}
     dev_data = {dt: torch.from_numpy(v).to(dev) for dt, v in data.items()}
     y64 = O.fill(N, O.F64, O.SEED, 6)
     y64d = torch.from_numpy(y64).to(dev)
@@ -45,9 +47,25 @@ def main():
         threads = int(rng.choice([32, 64, 96, 128, 256, 1024, int(rng.integers(1, 1025))]))
         lb = int(rng.integers(0, 100))
         ub = int(rng.integers(lb - 2, N))
-        kind = str(rng.choice(["sum64", "sum32", "max64", "min32", "dot", "axpy"]))
+        kind = str(rng.choice(["sum64", "sum32", "max64", "min32", "dot", "axpy",
+                               "spmd_i64", "spmd_u32max", "spmd_f64"]))
         kinds[kind] = kinds.get(kind, 0) + 1
-        if kind in ("sum64", "sum32", "max64", "min32"):
+        if kind.startswith("spmd"):
+            dt, op = {"spmd_i64": (O.I64, "add"), "spmd_u32max": (O.U32, "max"),
+                      "spmd_f64": (O.F64, "add")}[kind]
+            init = 0
+            want = O.reduce(data[dt], lb, ub, dt, O.ADD if op == "add" else O.MAX,
+                            SCHEDS[sched], chunk, teams, threads, init)
+            out = torch.zeros(1, dtype=dev_data[dt].dtype, device=dev)
+            runtime.reduce(dev_data[dt], op, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                           threads=threads, out=out)
+            got = out.cpu().numpy()[0]
+            if dt == O.F64:
+                ex = O.accurate_sum_f64(data[dt][lb:ub + 1]) if ub >= lb else 0.0
+                ok = abs(float(got) - ex) <= 1e-6 * max(abs(ex), 1e-30)
+            else:
+                ok = int(got) == int(want)
+        elif kind in ("sum64", "sum32", "max64", "min32"):
             dt = O.F64 if kind.endswith("64") else O.F32
             op = {"sum": "add", "max": "max", "min": "min"}[kind[:3]]
             init = {"add": 0.0, "max": -np.inf, "min": np.inf}[op]
