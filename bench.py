@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--teams", type=int, default=0, help="0: one team per SM")
-    p.add_argument("--threads", type=int, default=256)
+    p.add_argument("--threads", type=int, default=384)
     p.add_argument("--sched", default="distribute")
     p.add_argument("--unroll", type=int, default=0)
     p.add_argument("--e2e-steps", type=int, default=3)

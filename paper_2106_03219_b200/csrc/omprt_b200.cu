@@ -165,12 +165,15 @@ inline int ord_grid(int teams, int threads, int nw) {
   return (int)(g < 1 ? 1 : g);
 }
 
-// streaming warps per CTA: enough that every SM gets work, at most 8
+// streaming warps per CTA: enough that every SM gets work; at most 8 (three
+// 256-byte stages each), or up to 12 (two stages) when that puts every group
+// in flight at once (e.g. 148 x 384 OpenMP threads: 12 groups per SM)
 inline int ord_default_nw(int teams, int threads) {
   const int64_t groups = ((int64_t)teams * threads + 31) / 32;
   const int sms = sm_count() > 0 ? sm_count() : 148;
   int64_t nw = (groups + sms - 1) / sms;
-  return (int)(nw < 1 ? 1 : (nw > 8 ? 8 : nw));
+  if (nw > 8) nw = nw <= 12 ? nw : 8;
+  return (int)(nw < 1 ? 1 : nw);
 }
 
 // Segments per group for the dynamic (load-balanced) ORDERED walk: block

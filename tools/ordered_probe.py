@@ -37,7 +37,8 @@ def main():
     dev = torch.device("cuda", 0)
     n = 1 << args.n
     x = runtime.synthetic(n, "f64", SEED, 0, device=dev)
-    cases = [("distribute", 1, 148, 256), ("distribute", 1, 148, 1024), ("static", 1, 148, 1024),
+    cases = [("distribute", 1, 148, 256), ("distribute", 1, 148, 384), ("distribute", 1, 148, 320),
+             ("distribute", 1, 148, 1024), ("static", 1, 148, 1024),
              ("static", 1, 296, 512), ("distribute_chunked", 4096, 148, 1024),
              ("static_chunked", 64, 148, 256)]
     for sched, chunk, teams, threads in cases:
