@@ -96,13 +96,18 @@ class Grid:
     threads: int
 
 
-def default_grid(device: torch.device | None = None, threads: int = 256,
+DEFAULT_THREADS = int(os.environ.get("OMPRT_DEFAULT_THREADS", "384"))
+
+
+def default_grid(device: torch.device | None = None, threads: int | None = None,
                  teams_per_sm: int = 1) -> Grid:
-    """A persistent grid: teams_per_sm resident teams on every SM (one
-    256-thread team per SM holds the 128 KiB bulk-copy ring)."""
+    """A persistent grid: teams_per_sm resident teams on every SM (one team
+    per SM holds the 128 KiB bulk-copy ring; 384 threads = 1 producer + 11
+    consumer warps, which keep the ring drained when the power cap lowers
+    the SM clock — profiles/r1_threads_sweep_256_384.txt)."""
     if device is not None:
         _lib.ensure_device(device.index or 0)
-    return Grid(num_sms() * teams_per_sm, threads)
+    return Grid(num_sms() * teams_per_sm, threads or DEFAULT_THREADS)
 
 
 # ------------------------------------------------------------------ trap

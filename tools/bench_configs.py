@@ -103,7 +103,7 @@ def main():
     line("C1 int64 sum static 1x128 N=2^20", ms, n * 8, cpu=c1,
          note="one OpenMP team split over 16 CTAs (team_set_cta); L2-resident after the first pass")
     ms = timeit(lambda: runtime.reduce(x, out=out), a.reps)
-    line("C1 int64 sum N=2^20, default grid", ms, n * 8, teams=sms, threads=256,
+    line("C1 int64 sum N=2^20, default grid", ms, n * 8, teams=sms, threads=runtime.DEFAULT_THREADS,
          note="L2-resident after the first pass")
     del x
 
@@ -116,17 +116,20 @@ def main():
     if CPU["on"]:
         ns = 1 << 26
         xh = O.fill(ns, O.F64, SEED)
-        c2 = cpu_ref(lambda: O.reduce(xh, 0, ns - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, sms, 256),
+        c2 = cpu_ref(lambda: O.reduce(xh, 0, ns - 1, O.F64, O.ADD, O.DISTRIBUTE, 1, sms,
+                                     runtime.DEFAULT_THREADS),
                      ns * 8)
-    line("C2 fp64 sum distribute SPMD N=2^30", ms, n * 8, cpu=c2, teams=sms, threads=256)
+    line("C2 fp64 sum distribute SPMD N=2^30", ms, n * 8, cpu=c2, teams=sms,
+         threads=runtime.DEFAULT_THREADS)
     for sched in ("static", "distribute_chunked", "static_chunked"):
         ms = timeit(lambda: runtime.reduce(x, sched=sched, chunk=64, out=outf), a.reps // 4)
-        line(f"C2 fp64 sum {sched} chunk=64 N=2^30", ms, n * 8, teams=sms, threads=256)
+        line(f"C2 fp64 sum {sched} chunk=64 N=2^30", ms, n * 8, teams=sms,
+             threads=runtime.DEFAULT_THREADS)
     xi = x.view(torch.int64)
     outi = torch.zeros(1, dtype=torch.int64, device=dev)
     ms = timeit(lambda: runtime.reduce(xi, "max", out=outi), a.reps // 4)
     line("C2-int int64 max N=2^30", ms, n * 8)
-    for thr in (1024, 256):
+    for thr in (1024, 384, 256):
         ms = timeit(lambda: runtime.reduce(x, mode="ordered", teams=sms, threads=thr, out=outf),
                     10, 1)
         line("C2 fp64 sum ORDERED (reference order, bit-exact) N=2^30", ms, n * 8,
@@ -139,8 +142,10 @@ def main():
     if CPU["on"]:
         ns = 1 << 25
         xh, yh = O.fill(ns, O.F64, SEED, 0), O.fill(ns, O.F64, SEED, 1)
-        c5 = cpu_ref(lambda: O.dot(xh, yh, 0, ns - 1, O.DISTRIBUTE, 1, sms, 256), ns * 16)
-    line("C5 fp64 dot N=2^30 per GPU shard", ms, n * 16, cpu=c5, teams=sms, threads=256)
+        c5 = cpu_ref(lambda: O.dot(xh, yh, 0, ns - 1, O.DISTRIBUTE, 1, sms,
+                                     runtime.DEFAULT_THREADS), ns * 16)
+    line("C5 fp64 dot N=2^30 per GPU shard", ms, n * 16, cpu=c5, teams=sms,
+         threads=runtime.DEFAULT_THREADS)
     del x, y, xi
     torch.cuda.empty_cache()
 
@@ -160,7 +165,8 @@ def main():
                 xh, yh = O.fill(ns, O.F32, SEED, 0), O.fill(ns, O.F32, SEED, 1)
                 code = {"distribute_chunked": O.DISTRIBUTE_CHUNKED,
                         "static_chunked": O.STATIC_CHUNKED}[sched]
-                c3 = cpu_ref(lambda: O.axpy_minmax(1e-7, xh, yh, 0, ns - 1, code, chunk, sms, 256,
+                c3 = cpu_ref(lambda: O.axpy_minmax(1e-7, xh, yh, 0, ns - 1, code, chunk, sms,
+                                                   runtime.DEFAULT_THREADS,
                                                    float("-inf"), float("inf")), ns * 12)
             line(f"C3 axpy+max/min {sched} chunk={chunk} N=2^28", ms, n * 12, cpu=c3)
     del xs, ys
