@@ -210,7 +210,12 @@ enum : int { kWorkExit = 0, kWorkRegion = 1 };
 
 constexpr uint32_t kBarFork = 1, kBarRegion = 2, kBarJoin = 3;
 
-template <class T, int OP, int U>
+// ORD: the ORDERED instance (its in-order worker loop needs more registers;
+// keeping it out of the SPMD instance keeps that one at 4 teams per SM).
+// TRACE: the instance with the trace-ring hooks, launched only while a ring
+// is installed (the hooks cost this kernel's short teams 4-6 % otherwise,
+// profiles/README.md).
+template <class T, int OP, int U, bool ORD = false, bool TRACE = false>
 __global__ void __launch_bounds__(kMaxThreads)
     k_generic(const T *__restrict__ x, int64_t lb, int64_t ub, int P, int ordered, int64_t pad,
               ArenaCfg cfg, Workspace ws, T *out, int64_t *team_offsets) {
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   __shared__ uint64_t s_off;
   const uint32_t nall = 32u + (uint32_t)P;
   const uint32_t lane = lane_id();
-  trace_begin();
+  if constexpr (TRACE) trace_begin();
 
   if (warp_id() == 0) {
     // ------------------------------------------------ main warp (sequential part)
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       if (lane == 0) {
         T *parts = (T *)arena_ptr(st, s_off);
         T v = Red<OP, T>::identity();
-        if (ordered) {
+        if constexpr (ORD) {
           for (int w = 0; w < P; ++w) v = Red<OP, T>::apply(v, parts[w]);
         } else {
           v = parts[P];
@@ -274,13 +279,15 @@ __global__ void __launch_bounds__(kMaxThreads)
       fence_acq_rel_gpu();
       const uint32_t t = atomic_inc_acq_rel_gpu(ws.ticket, gridDim.x - 1);
       last = t == gridDim.x - 1;
-      trace_record(blockIdx.x, kTraceTeam, t, trace_t0());
-      if (last) trace_t0() = globaltimer();
+      if constexpr (TRACE) {
+        trace_record(blockIdx.x, kTraceTeam, t, trace_t0());
+        if (last) trace_t0() = globaltimer();
+      }
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
       fence_acq_rel_gpu();
-      if (ordered) {
+      if constexpr (ORD) {
         if (lane == 0 && !trap_raised())
           *out = fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x);
       } else {
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         v = warp_reduce<OP, T>(v, 32);
         if (lane == 0 && !trap_raised()) *out = Red<OP, T>::apply(*out, v);
       }
-      trace_combine();
+      if constexpr (TRACE) trace_combine();
     }
   } else {
     // ------------------------------------------------ worker state machine
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       if (s_work == kWorkExit) break;
       T *parts = (T *)arena_ptr(st, s_off);
       const int64_t tlb = s_tlb, tub = s_tub;
-      if (ordered) {
+      if constexpr (ORD) {
         // for_static_init over the team block, literal sequential chunk
         int64_t mlb, mub;
         static_bounds(tlb, tub, wt, P, mlb, mub);

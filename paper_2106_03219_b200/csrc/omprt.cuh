@@ -392,7 +392,10 @@ struct TraceRing {
   TraceRec *recs;
   uint32_t cap;
 };
-__device__ TraceRing g_trace;
+// constant bank: every CTA reads it at start and end, so it must cost nothing
+// when no ring is installed (a global would put an L2 round trip on each
+// short team's critical path)
+__constant__ TraceRing g_trace;
 
 OMPRT_D uint64_t globaltimer() {
   uint64_t t;

@@ -51,6 +51,7 @@ inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 int g_unroll = 4;   // tuning knob: vectors in flight per lane per iteration
 int g_variant = 0;  // tuning knob: kernel variant of the fp64 sum (0 = default)
 constexpr int kOrderedLiteral = 20;  // variant: ORDERED mode through the literal walk
+bool g_trace_on = false;  // a trace ring is installed (selects traced kernel instances)
 
 int check_grid(int teams, int threads) {
   if (teams < 1) return fail(OMPRT_EINVAL, "teams must be >= 1 (got %d)", teams);
@@ -436,10 +437,12 @@ template <class T, int OP>
 int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, int ordered,
                      int64_t pad, ArenaCfg cfg, Workspace w, void *out, int64_t *offs,
                      cudaStream_t st) {
-  auto kern = k_generic<T, OP, 4>;
-  // integer folds give the same bits in any order (see launch_reduce_t):
-  // the ordered worker loop is only needed for fp
-  if (std::is_integral<T>::value && g_variant != kOrderedLiteral) ordered = 0;
+  // the ORDERED instance only where order matters (fp): integer folds give
+  // the same bits in any order (see launch_reduce_t) and take the SPMD one
+  auto kern = g_trace_on ? k_generic<T, OP, 4, false, true> : k_generic<T, OP, 4, false>;
+  if constexpr (std::is_floating_point<T>::value) {
+    if (ordered) kern = g_trace_on ? k_generic<T, OP, 4, true, true> : k_generic<T, OP, 4, true>;
+  }
   // Physical backing of the team arena: the region's known allocation
   // footprint (pad, then parts[P+1]) capped at the semantic capacity.  The
   // overflow check still uses cfg.capacity (64 KiB, the reference's
@@ -630,6 +633,7 @@ int omprt_set_trace(void *d_records, int64_t capacity) {
   r.recs = capacity > 0 ? reinterpret_cast<TraceRec *>(d_records) : nullptr;
   r.cap = (uint32_t)(capacity > 0xffffffffll ? 0xffffffffll : capacity);
   OMPRT_CUDA(cudaMemcpyToSymbol(g_trace, &r, sizeof(r)));
+  g_trace_on = r.recs != nullptr;
   return OMPRT_OK;
 }
 

@@ -83,3 +83,17 @@ def test_tgt_target_collect_trace(cuda):
     assert int(np.frombuffer(bytes(cell), dtype=np.int64)[0]) == int(x.sum())
     kinds = [ln.split()[3] for ln in out["trace"]]
     assert kinds.count("atomic.inc") >= 4 and kinds[-1] == "combine"
+
+
+def test_generic_mode_records_while_traced(cuda):
+    # generic mode launches its traced instance only while a ring is installed
+    x = runtime.synthetic(1 << 20, "i64", O.SEED, device=cuda)
+    with runtime.Trace(cuda) as tr:
+        runtime.generic_reduce(x, teams=64, par_threads=128)
+    teams = tr.records[tr.records["kind"] == 1]
+    assert len(teams) == 64 and sorted(teams["ticket"].tolist()) == list(range(64))
+    assert len(tr.records[tr.records["kind"] == 2]) == 1
+    after = runtime.Trace(cuda)
+    runtime.generic_reduce(x, teams=64, par_threads=128)
+    torch.cuda.synchronize()
+    assert int(after.buf.abs().sum().item()) == 0
