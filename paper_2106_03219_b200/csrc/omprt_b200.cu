@@ -12,6 +12,7 @@
 #include <mutex>
 #include <string>
 #include <type_traits>
+#include <unordered_map>
 
 #include "bulk.cuh"
 #include "generic.cuh"
@@ -71,11 +72,28 @@ int check_sched(int sched, int64_t chunk) {
 
 // ---------------------------------------------------------------- dispatch
 
+// The dynamic-smem opt-in is per (device, kernel) and sticky: set it once,
+// not on every launch (the call costs ~microseconds, visible on short
+// constructs such as config 1).
+std::mutex g_smem_mu;
+std::unordered_map<uint64_t, size_t> g_smem_set;
+
 template <class K> int set_smem(K kern, size_t bytes) {
   if (bytes <= 48 * 1024) return OMPRT_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = ((uint64_t)dev << 56) ^ (uint64_t)(uintptr_t)(const void *)kern;
+  {
+    std::lock_guard<std::mutex> lk(g_smem_mu);
+    auto it = g_smem_set.find(key);
+    if (it != g_smem_set.end() && it->second >= bytes) return OMPRT_OK;
+  }
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return fail(OMPRT_ECUDA, "smem attribute: %s", cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(g_smem_mu);
+  size_t &v = g_smem_set[key];
+  if (v < bytes) v = bytes;
   return OMPRT_OK;
 }
 
