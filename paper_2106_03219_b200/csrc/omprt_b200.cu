@@ -146,16 +146,18 @@ int sm_count() {
 }
 
 // SPMD launches with few teams split every team over `split` CTAs
-// (team_set_cta) so the whole GPU streams: split = SMs / teams (<= 16) when
-// teams <= SMs / 2.  Variant kNoSplit keeps one CTA per team.
+// (team_set_cta) so the whole GPU streams: split = SMs / teams when
+// teams <= SMs / 2 (teams * split <= SMs <= kMinPartialSlots).  Config 1
+// (1 team x 128 threads, 2^20 int64): 148 CTAs 15.7 us, 16 CTAs 22.6 us,
+// unsplit 240 us (profiles/r1_c1_split.jsonl).  Variant kNoSplit keeps one
+// CTA per team.
 constexpr int kNoSplit = 30;
 
 int spmd_split(int teams) {
   if (g_variant == kNoSplit) return 1;
   const int sms = sm_count();
   if (sms <= 0 || teams * 2 > sms) return 1;
-  int cl = sms / teams;
-  return cl > 16 ? 16 : cl;
+  return sms / teams;
 }
 
 // ORDERED row-group kernels (ordered.cuh).  Each CTA = nw streaming warps +

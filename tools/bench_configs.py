@@ -101,7 +101,7 @@ def main():
         xh = O.fill(n, O.I64, SEED)
         c1 = cpu_ref(lambda: O.reduce(xh, 0, n - 1, O.I64, O.ADD, O.STATIC, 1, 1, 128), n * 8)
     line("C1 int64 sum static 1x128 N=2^20", ms, n * 8, cpu=c1,
-         note="one OpenMP team split over 16 CTAs (team_set_cta); L2-resident after the first pass")
+         note="one OpenMP team split over 148 CTAs (team_set_cta); L2-resident after the first pass")
     ms = timeit(lambda: runtime.reduce(x, out=out), a.reps)
     line("C1 int64 sum N=2^20, default grid", ms, n * 8, teams=sms, threads=runtime.DEFAULT_THREADS,
          note="L2-resident after the first pass")
