@@ -17,5 +17,8 @@ for dtype in ("i64", "f64"):
     for ordered in (False, True):
         ms = timeit(lambda: runtime.generic_reduce(x, teams=1024, par_threads=256, ordered=ordered,
                                                    out=o), 100)
-        print(json.dumps({"dtype": dtype, "ordered": ordered, "gbs": round(n * 8 / ms / 1e6, 1)}),
-              flush=True)
+        o.zero_()
+        runtime.generic_reduce(x, teams=1024, par_threads=256, ordered=ordered, out=o)
+        bits = o.view(torch.int64).item()
+        print(json.dumps({"dtype": dtype, "ordered": ordered, "gbs": round(n * 8 / ms / 1e6, 1),
+                          "bits": hex(bits & (2**64 - 1))}), flush=True)
