@@ -170,7 +170,7 @@ class PeerExchange:
             _lib.OP_NAMES[op], _lib.SCHED_NAMES[sched], chunk, teams, threads,
             C.c_void_p(ws.data_ptr()), C.c_void_p(out.data_ptr()),
             C.c_void_p(self.peers.data_ptr()), self.rank, self.world, key, self.step,
-            C.c_void_p(torch.cuda.current_stream(x_shard.device).cuda_stream)),
+            C.c_void_p(runtime.stream_handle(x_shard.device))),
             "omprt_reduce_exchange")
         self.step += 1
         return out

@@ -52,8 +52,21 @@ def _code(table: dict, v) -> int:
     return v if isinstance(v, int) else table[v]
 
 
+# the current stream's raw handle without building a torch.cuda.Stream object
+# (the wrapper is most of a small launch's host time: profiles/r1_c1_host.json)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def stream_handle(device: torch.device) -> int:
+    """cudaStream_t of the current stream on `device`, as an int."""
+    if _raw_stream is not None:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        return _raw_stream(idx)
+    return torch.cuda.current_stream(device).cuda_stream
+
+
 def _stream(t: torch.Tensor) -> C.c_void_p:
-    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    return C.c_void_p(stream_handle(t.device))
 
 
 def _dev(t: torch.Tensor) -> torch.device:
@@ -70,9 +83,10 @@ def _p(t: torch.Tensor | None) -> C.c_void_p:
 _sms: dict[int, int] = {}
 
 
-def num_sms() -> int:
-    """SM count of the current CUDA device (cached per device)."""
-    dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+def num_sms(index: int | None = None) -> int:
+    """SM count of CUDA device `index` (default: the current one), cached."""
+    dev = index if index is not None else (
+        torch.cuda.current_device() if torch.cuda.is_available() else -1)
     n = _sms.get(dev)
     if n is None:
         n = _sms[dev] = check(_lib.load().omprt_num_sms(), "omprt_num_sms")
@@ -107,6 +121,7 @@ def default_grid(device: torch.device | None = None, threads: int | None = None,
     the SM clock — profiles/r1_threads_sweep_256_384.txt)."""
     if device is not None:
         _lib.ensure_device(device.index or 0)
+        return Grid(num_sms(device.index) * teams_per_sm, threads or DEFAULT_THREADS)
     return Grid(num_sms() * teams_per_sm, threads or DEFAULT_THREADS)
 
 
@@ -247,7 +262,7 @@ def workspace(device: torch.device, nbytes: int) -> torch.Tensor:
     """Zeroed device workspace, cached per (device, stream): the
     last-team-finishes ticket self-resets, so launches ordered on one stream
     may share it; concurrent streams each get their own."""
-    key = (device.type, device.index or 0, torch.cuda.current_stream(device).cuda_stream)
+    key = (device.type, device.index or 0, stream_handle(device))
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
@@ -255,8 +270,15 @@ def workspace(device: torch.device, nbytes: int) -> torch.Tensor:
     return ws
 
 
+_ws_bytes: dict[tuple, int] = {}
+
+
 def reduce_workspace(device: torch.device, teams: int, threads: int, mode: int) -> torch.Tensor:
-    return workspace(device, _lib.load().omprt_reduce_workspace_bytes(teams, threads, mode))
+    key = (teams, threads, mode)
+    nb = _ws_bytes.get(key)
+    if nb is None:
+        nb = _ws_bytes[key] = _lib.load().omprt_reduce_workspace_bytes(teams, threads, mode)
+    return workspace(device, nb)
 
 
 # ---------------------------------------------------------------- reduce

@@ -1,4 +1,4 @@
-"""Config 1 (int64 sum, 1 team x 128 threads, 2^20) back-to-back time vs the split cap."""
+"""Config 1 (int64 sum, 1 team x 128 threads, 2^20) back-to-back time, team split on/off."""
 import json
 import sys
 from pathlib import Path
@@ -15,7 +15,7 @@ x = runtime.synthetic(n, "i64", 0x210603219, device=dev)
 out = torch.zeros(1, dtype=torch.int64, device=dev)
 want = None
 for rep in range(2):
-    for var, name in ((30, "no split"), (0, "cap 16"), (35, "cap 64"), (36, "cap 148")):
+    for var, name in ((30, "no split"), (0, "split over all SMs")):
         runtime.set_variant(var)
         ms = timeit(lambda: runtime.reduce(x, teams=1, threads=128, out=out), 300)
         out.zero_()
