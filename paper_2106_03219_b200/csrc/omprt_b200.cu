@@ -234,11 +234,20 @@ int launch_ordered_rows(const T *xp, LoopArgs la, int teams, int threads, int nw
   return check_launch("omprt_reduce(ordered rows)");
 }
 
-// Default ORDERED policy: 512-byte row windows when three stages fit, else
-// 256-byte windows.
+// Default ORDERED policy: six warps with 512-byte row windows (two stages)
+// when the groups per SM come in whole waves of six or are many (>= 24);
+// else 512-byte windows when three stages fit, else 256-byte windows.
+// Measured (profiles/r1_ordered_sweep_windows.jsonl): 148 x 384 threads
+// 5.53 vs 5.18 TB/s, distribute_chunked 148 x 1024 5.50 vs 5.28; 8 or 16
+// groups per SM lose a partial wave with six warps (4.1 / 5.2 vs 5.4).
 template <class T, int OP>
 int launch_ordered_default(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
                            cudaStream_t st) {
+  const int64_t groups = ((int64_t)teams * threads + 31) / 32;
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t per_sm = (groups + sms - 1) / sms;
+  if ((per_sm % 6 == 0 || per_sm >= 24) && OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(6) >= 2)
+    return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 6, w, op, st);
   const int nw = ord_default_nw(teams, threads);
   if (OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(nw) >= 3)
     return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, nw, w, op, st);
@@ -257,6 +266,9 @@ int launch_ordered_variant(int v, const T *xp, LoopArgs la, int teams, int threa
     case 25: return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 2, w, op, st);
     case 26: return launch_ordered_rows<T, OP, 256>(xp, la, teams, threads, 12, w, op, st);
     case 27: return launch_ordered_rows<T, OP, 128>(xp, la, teams, threads, 8, w, op, st);
+    case 28: return launch_ordered_rows<T, OP, 256>(xp, la, teams, threads, 6, w, op, st);
+    case 29: return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 6, w, op, st);
+    case 41: return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 5, w, op, st);
     default: return fail(OMPRT_EINVAL, "unknown ordered variant %d", v);
   }
 }

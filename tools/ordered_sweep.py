@@ -1,4 +1,5 @@
-"""Sweep the ORDERED fp64-sum variants (omprt_set_variant 0, 20..27) at 2^30."""
+"""Sweep the ORDERED fp64-sum variants (omprt_set_variant 0, 20..29, 41) at 2^30.
+    python tools/ordered_sweep.py [vars=0,22,29] [sched:chunk:teams:threads ...]"""
 import json
 import sys
 from pathlib import Path
@@ -12,11 +13,18 @@ from tools.ordered_probe import timed, SEED  # noqa: E402
 dev = torch.device("cuda", 0)
 n = 1 << 30
 x = runtime.synthetic(n, "f64", SEED, 0, device=dev)
-for sched, chunk, teams, threads in (("distribute", 1, 148, 256), ("distribute", 1, 148, 1024),
-                                     ("distribute", 1, 148, 128), ("distribute", 1, 296, 256),
-                                     ("static_chunked", 64, 148, 256)):
+GEOMS = (("distribute", 1, 148, 256), ("distribute", 1, 148, 1024),
+         ("distribute", 1, 148, 128), ("distribute", 1, 296, 256),
+         ("static_chunked", 64, 148, 256))
+VARS = (20, 31, 0, 21, 22, 23, 24, 25, 26, 27, 28, 29, 41)
+args = sys.argv[1:]
+if args and args[0].startswith("vars="):  # e.g. vars=0,22,29
+    VARS = tuple(int(v) for v in args.pop(0)[5:].split(","))
+if args:  # e.g. distribute:1:148:384
+    GEOMS = tuple((a, int(b), int(c), int(d)) for a, b, c, d in (g.split(":") for g in args))
+for sched, chunk, teams, threads in GEOMS:
     ref = None
-    for var in (20, 31, 0, 21, 22, 23, 24, 25, 26, 27):
+    for var in VARS:
         runtime.set_variant(var)
         out = torch.zeros(1, dtype=torch.float64, device=dev)
 
