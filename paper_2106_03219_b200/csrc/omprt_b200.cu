@@ -197,6 +197,15 @@ inline int ord_default_nw(int teams, int threads) {
   return (int)(nw < 1 ? 1 : nw);
 }
 
+// Six streaming warps fill whole waves when the 32-thread groups per SM are
+// a multiple of six or many (launch_ordered_default).
+inline bool ord_six_warps(int teams, int threads) {
+  const int64_t groups = ((int64_t)teams * threads + 31) / 32;
+  const int sms = sm_count() > 0 ? sm_count() : 148;
+  const int64_t per_sm = (groups + sms - 1) / sms;
+  return per_sm % 6 == 0 || per_sm >= 24;
+}
+
 // Segments per group for the dynamic (load-balanced) ORDERED walk: block
 // schedules only, ~64+ windows per unit, at most 8 units per group;
 // omprt_set_variant(31) keeps the static assignment.
@@ -243,10 +252,7 @@ int launch_ordered_rows(const T *xp, LoopArgs la, int teams, int threads, int nw
 template <class T, int OP>
 int launch_ordered_default(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
                            cudaStream_t st) {
-  const int64_t groups = ((int64_t)teams * threads + 31) / 32;
-  const int sms = sm_count() > 0 ? sm_count() : 148;
-  const int64_t per_sm = (groups + sms - 1) / sms;
-  if ((per_sm % 6 == 0 || per_sm >= 24) && OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(6) >= 2)
+  if (ord_six_warps(teams, threads) && OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(6) >= 2)
     return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 6, w, op, st);
   const int nw = ord_default_nw(teams, threads);
   if (OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(nw) >= 3)
@@ -822,7 +828,10 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
   const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
   if (mode == OMPRT_MODE_ORDERED) {
     if (g_variant != kOrderedLiteral && ord_rows_ok(la, d_x, d_y)) {
-      const int nw = ord_default_nw(teams, threads);
+      // six warps when they fill whole waves: two streams' 256-byte windows
+      // then fit two stages (148 x 384: 3.9 -> 5.7 TB/s; static_chunked 64:
+      // 2.1 -> 6.1, profiles/r1_ordered_six_dot.jsonl)
+      const int nw = ord_six_warps(teams, threads) ? 6 : ord_default_nw(teams, threads);
       const int s512 = OrdSmem<double, 64, 2>::stages_for(nw);
       const int s256 = OrdSmem<double, 32, 2>::stages_for(nw);
       const int s128 = OrdSmem<double, 16, 2>::stages_for(nw);
