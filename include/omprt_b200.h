@@ -139,7 +139,8 @@ int omprt_set_unroll(int unroll);
  * variants; 10-16 TMA bulk-copy (cp.async.bulk + mbarrier) stage rings;
  * 20 = ORDERED mode through the literal per-thread walk instead of the
  * row-group kernels (cp.async shared-memory row windows + folder warp);
- * 21-29 = row-group kernels with a forced window size x warps per SM;
+ * 21-29, 41 = row-group kernels with a forced window size x warps per SM;
+ * 44 = ORDERED without the six-warp window policy;
  * 30 = SPMD without splitting few teams over several CTAs; 31 = ORDERED
  * row-group kernels with the static group assignment (no dynamic segments). */
 int omprt_set_variant(int variant);

@@ -198,12 +198,14 @@ inline int ord_default_nw(int teams, int threads) {
 }
 
 // Six streaming warps fill whole waves when the 32-thread groups per SM are
-// a multiple of six or many (launch_ordered_default).
-inline bool ord_six_warps(int teams, int threads) {
+// a multiple of six (up to `whole_max` groups per SM), or are many (>= `many`).
+constexpr int kOrderedNoSix = 44;  // variant: never the six-warp policy (A/B)
+inline bool ord_six_warps(int teams, int threads, int64_t whole_max, int64_t many) {
+  if (g_variant == kOrderedNoSix) return false;
   const int64_t groups = ((int64_t)teams * threads + 31) / 32;
   const int sms = sm_count() > 0 ? sm_count() : 148;
   const int64_t per_sm = (groups + sms - 1) / sms;
-  return per_sm % 6 == 0 || per_sm >= 24;
+  return (per_sm % 6 == 0 && per_sm <= whole_max) || per_sm >= many;
 }
 
 // Segments per group for the dynamic (load-balanced) ORDERED walk: block
@@ -244,15 +246,18 @@ int launch_ordered_rows(const T *xp, LoopArgs la, int teams, int threads, int nw
 }
 
 // Default ORDERED policy: six warps with 512-byte row windows (two stages)
-// when the groups per SM come in whole waves of six or are many (>= 24);
+// when the groups per SM come in whole waves of six (6, 12 or 18 per SM);
 // else 512-byte windows when three stages fit, else 256-byte windows.
-// Measured (profiles/r1_ordered_sweep_windows.jsonl): 148 x 384 threads
-// 5.53 vs 5.18 TB/s, distribute_chunked 148 x 1024 5.50 vs 5.28; 8 or 16
-// groups per SM lose a partial wave with six warps (4.1 / 5.2 vs 5.4).
+// Measured: 148 x 384 threads 5.53 vs 5.18 TB/s isolated
+// (profiles/r1_ordered_sweep_windows.jsonl) and 5.49-5.59 vs 5.10-5.13 in
+// the power-capped steady state (profiles/r1_ordered_steady_ab.jsonl), where
+// 24 and 32 groups per SM gain nothing (-2 % at 148 x 1024); 8 or 16 groups
+// per SM lose a partial wave with six warps (4.1 / 5.2 vs 5.4).
 template <class T, int OP>
 int launch_ordered_default(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
                            cudaStream_t st) {
-  if (ord_six_warps(teams, threads) && OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(6) >= 2)
+  if (ord_six_warps(teams, threads, 18, INT64_MAX) &&
+      OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(6) >= 2)
     return launch_ordered_rows<T, OP, 512>(xp, la, teams, threads, 6, w, op, st);
   const int nw = ord_default_nw(teams, threads);
   if (OrdSmem<T, 512 / (int)sizeof(T), 1>::stages_for(nw) >= 3)
@@ -831,7 +836,7 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
       // six warps when they fill whole waves: two streams' 256-byte windows
       // then fit two stages (148 x 384: 3.9 -> 5.7 TB/s; static_chunked 64:
       // 2.1 -> 6.1, profiles/r1_ordered_six_dot.jsonl)
-      const int nw = ord_six_warps(teams, threads) ? 6 : ord_default_nw(teams, threads);
+      const int nw = ord_six_warps(teams, threads, INT64_MAX, 24) ? 6 : ord_default_nw(teams, threads);
       const int s512 = OrdSmem<double, 64, 2>::stages_for(nw);
       const int s256 = OrdSmem<double, 32, 2>::stages_for(nw);
       const int s128 = OrdSmem<double, 16, 2>::stages_for(nw);
