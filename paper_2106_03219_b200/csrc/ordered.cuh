@@ -451,6 +451,31 @@ OMPRT_D void ord_folder_load(const T *tp, int64_t P, const uint64_t *flags, uint
   for (int k = 0; k < N; ++k) L.v[k] = (first + k < P) ? ld_cg(tp + first + k) : T();
 }
 
+template <class T> OMPRT_D T shfl_any(T v, int src_or_delta, bool down) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte partials");
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long u;
+    memcpy(&u, &v, 8);
+    u = down ? __shfl_down_sync(0xffffffffu, u, src_or_delta) : __shfl_sync(0xffffffffu, u, src_or_delta);
+    memcpy(&v, &u, 8);
+  } else {
+    unsigned u;
+    memcpy(&u, &v, 4);
+    u = down ? __shfl_down_sync(0xffffffffu, u, src_or_delta) : __shfl_sync(0xffffffffu, u, src_or_delta);
+    memcpy(&v, &u, 4);
+  }
+  return v;
+}
+
+// The folder warp: folds the P per-thread partials in global thread order
+// into acc.  For max/min (Combine::kAssoc) the reference's step
+// `acc < e ? e : acc` keeps the leftmost maximum of its operands (a partial
+// is never NaN: it starts at the identity and only ever takes an e that
+// compares greater; ±0 tie and the left one stays), which is associative —
+// so a full batch folds as a left-biased tree (each lane its 8 partials in
+// order, then lane i takes lane i+d for d = 1..16) with the sequential
+// fold's exact bits; a NaN cell value stays absorbing because acc is
+// combined last.  Sums fold strictly one by one.
 template <class T, class Combine>
 OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epoch, T acc,
                      T *ring, Combine &&comb) {
@@ -473,8 +498,17 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
     __syncwarp();
     const int64_t base = b * kFoldPer;
     if (base + kFoldPer <= P) {
+      if constexpr (std::decay_t<Combine>::kAssoc) {
+        T v = cur[lane * N];
+#pragma unroll
+        for (int k = 1; k < N; ++k) v = comb(v, cur[lane * N + k]);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) v = comb(v, shfl_any<T>(v, d, true));
+        acc = comb(acc, shfl_any<T>(v, 0, false));
+      } else {
 #pragma unroll 32
-      for (int j = 0; j < kFoldPer; ++j) acc = comb(acc, cur[j]);
+        for (int j = 0; j < kFoldPer; ++j) acc = comb(acc, cur[j]);
+      }
     } else {
       for (int j = 0; base + j < P; ++j) acc = comb(acc, cur[j]);
     }
@@ -486,6 +520,7 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
 }
 
 template <int OP, class T> struct RedComb {
+  static constexpr bool kAssoc = OP != OMPRT_OP_ADD;  // leftmost max / min (ord_folder)
   OMPRT_D T operator()(T a, T b) const { return Red<OP, T>::apply(a, b); }
 };
 
@@ -587,6 +622,7 @@ template <int W> struct OrdMinMaxFold {
 };
 
 struct MinMaxComb {
+  static constexpr bool kAssoc = true;
   OMPRT_D float2 operator()(float2 a, float2 b) const {
     return make_float2(Red<OMPRT_OP_MAX, float>::apply(a.x, b.x),
                        Red<OMPRT_OP_MIN, float>::apply(a.y, b.y));

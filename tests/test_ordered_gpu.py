@@ -148,3 +148,49 @@ def test_ordered_ignores_stale_workspace_contents(cuda):
         got = _ordered(x, "add", "distribute", 1, 64, 320, 0, n - 1, 0.0)
         assert got == want, pattern
     runtime.reduce_workspace(cuda, 64, 320, 2).zero_()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("op", ["max", "min"])
+def test_ordered_maxmin_signed_zeros_and_nans(cuda, dtype, op):
+    """The folder folds max/min partials as a left-biased tree (ord_folder):
+    the reference step keeps the leftmost of tied values (-0 vs +0) and never
+    takes a NaN element, and a NaN cell stays NaN — all bit-exact against the
+    sequential order at geometries with many full folder batches."""
+    dt = DTS[dtype]
+    n = 1_000_003
+    rng = np.random.default_rng(11)
+    x = (-rng.random(n)).astype(np.float64 if dtype == "f64" else np.float32)
+    if op == "min":
+        x = -x
+    # the extreme value is a zero of either sign, scattered; NaNs sprinkled
+    zeros = rng.choice(n, 5000, replace=False)
+    x[zeros] = np.where(rng.random(5000) < 0.5, -0.0, 0.0)
+    x[rng.choice(n, 3000, replace=False)] = np.nan
+    xd = torch.from_numpy(x).to(cuda)
+    ident = -np.inf if op == "max" else np.inf
+    opc = O.MAX if op == "max" else O.MIN
+    for sched, chunk, teams, threads in (("static", 1, 148, 256), ("distribute", 1, 148, 384),
+                                         ("static_chunked", 64, 37, 1024)):
+        for init in (ident, np.nan):
+            want = O.reduce(x, 0, n - 1, dt, opc, SCHEDS[sched], chunk, teams, threads, init)
+            got = _ordered(xd, op, sched, chunk, teams, threads, 0, n - 1, init)
+            assert np.array([got]).tobytes() == np.array([want], dtype=x.dtype).tobytes(), \
+                (sched, teams, threads, init, got, want)
+
+
+def test_axpy_ordered_minmax_signed_zeros(cuda):
+    """C3 in ORDERED mode: the max/min pass's float2 folder (tree over full
+    batches) against the oracle when the extremes are signed zeros."""
+    n = 600_001
+    rng = np.random.default_rng(5)
+    x = np.full(n, -0.0, dtype=np.float32)  # fmaf(a, -0, y) keeps y's sign
+    y = np.where(rng.random(n) < 0.5, -0.0, 0.0).astype(np.float32)
+    y[rng.choice(n, 100, replace=False)] = 0.0
+    yo = y.copy()
+    mx, mn = O.axpy_minmax(0.75, x, yo, 0, n - 1, O.DISTRIBUTE, 1, 148, 1024, -np.inf, np.inf)
+    yd = torch.from_numpy(y).to(cuda)
+    gmx, gmn = runtime.axpy_minmax(0.75, torch.from_numpy(x).to(cuda), yd, sched="distribute",
+                                   teams=148, threads=1024, mode="ordered")
+    assert np.float32(gmx.item()).tobytes() == np.float32(mx).tobytes()
+    assert np.float32(gmn.item()).tobytes() == np.float32(mn).tobytes()
