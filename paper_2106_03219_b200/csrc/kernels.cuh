@@ -341,6 +341,32 @@ OMPRT_D T fold_in_order_team(T acc, const T *p, int64_t n, T *buf, int cap) {
     const int m = (int)((n - base) < cap ? (n - base) : cap);
     for (int k = threadIdx.x; k < m; k += blockDim.x) buf[k] = ld_cg(p + base + k);
     __syncthreads();
+    if constexpr (OP != OMPRT_OP_ADD) {
+      // max/min: the reference step keeps the leftmost of tied values and
+      // per-thread partials are never NaN, so the in-order fold equals a
+      // left-biased tree (see ord_folder, ordered.cuh): thread t folds the
+      // t-th contiguous slice from the identity (±inf, neutral), each warp
+      // combines lane i with lane i+d, thread 0 takes the warps in order.
+      const int seg = (m + (int)blockDim.x - 1) / (int)blockDim.x;
+      const int k0 = (int)threadIdx.x * seg;
+      T v = Red<OP, T>::identity();
+      for (int k = k0; k < k0 + seg && k < m; ++k) v = Red<OP, T>::apply(v, buf[k]);
+      const uint32_t lane = threadIdx.x & 31u, wb = threadIdx.x & ~31u;
+      const uint32_t lanes = blockDim.x - wb < 32u ? blockDim.x - wb : 32u;
+      const uint32_t mask = lanes == 32u ? 0xffffffffu : ((1u << lanes) - 1u);
+#pragma unroll
+      for (uint32_t d = 1; d < 32; d <<= 1) {
+        const T o = __shfl_down_sync(mask, v, d);
+        if (lane + d < lanes) v = Red<OP, T>::apply(v, o);
+      }
+      __syncthreads();  // every thread is done reading buf
+      if (lane == 0) buf[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (uint32_t w = 0; w < (blockDim.x + 31u) / 32u; ++w) acc = Red<OP, T>::apply(acc, buf[w]);
+      __syncthreads();
+      continue;
+    }
     if (threadIdx.x == 0) {
       int k = 0;
       for (; k + 8 <= m; k += 8) {

@@ -170,13 +170,19 @@ def test_ordered_maxmin_signed_zeros_and_nans(cuda, dtype, op):
     xd = torch.from_numpy(x).to(cuda)
     ident = -np.inf if op == "max" else np.inf
     opc = O.MAX if op == "max" else O.MIN
-    for sched, chunk, teams, threads in (("static", 1, 148, 256), ("distribute", 1, 148, 384),
-                                         ("static_chunked", 64, 37, 1024)):
-        for init in (ident, np.nan):
-            want = O.reduce(x, 0, n - 1, dt, opc, SCHEDS[sched], chunk, teams, threads, init)
-            got = _ordered(xd, op, sched, chunk, teams, threads, 0, n - 1, init)
-            assert np.array([got]).tobytes() == np.array([want], dtype=x.dtype).tobytes(), \
-                (sched, teams, threads, init, got, want)
+    cases = (("static", 1, 148, 256, 0), ("distribute", 1, 148, 384, 0),
+             ("static_chunked", 64, 37, 1024, 0), ("static_chunked", 7, 148, 256, 0),
+             ("distribute", 1, 148, 384, LITERAL), ("static", 1, 67, 1000, LITERAL))
+    try:
+        for sched, chunk, teams, threads, variant in cases:
+            runtime.set_variant(variant)  # LITERAL: the literal walk's team combine
+            for init in (ident, np.nan):
+                want = O.reduce(x, 0, n - 1, dt, opc, SCHEDS[sched], chunk, teams, threads, init)
+                got = _ordered(xd, op, sched, chunk, teams, threads, 0, n - 1, init)
+                assert np.array([got]).tobytes() == np.array([want], dtype=x.dtype).tobytes(), \
+                    (sched, chunk, teams, threads, variant, init, got, want)
+    finally:
+        runtime.set_variant(0)
 
 
 def test_axpy_ordered_minmax_signed_zeros(cuda):
@@ -192,5 +198,15 @@ def test_axpy_ordered_minmax_signed_zeros(cuda):
     yd = torch.from_numpy(y).to(cuda)
     gmx, gmn = runtime.axpy_minmax(0.75, torch.from_numpy(x).to(cuda), yd, sched="distribute",
                                    teams=148, threads=1024, mode="ordered")
+    assert np.float32(gmx.item()).tobytes() == np.float32(mx).tobytes()
+    assert np.float32(gmn.item()).tobytes() == np.float32(mn).tobytes()
+    # chunk 1: the literal walk (k_axpy_minmax_ordered) and its team combine
+    yo = y.copy()
+    mx, mn = O.axpy_minmax(0.75, x, yo, 0, n - 1, O.DISTRIBUTE_CHUNKED, 1, 148, 384, -np.inf,
+                           np.inf)
+    yd = torch.from_numpy(y).to(cuda)
+    gmx, gmn = runtime.axpy_minmax(0.75, torch.from_numpy(x).to(cuda), yd,
+                                   sched="distribute_chunked", chunk=1, teams=148, threads=384,
+                                   mode="ordered")
     assert np.float32(gmx.item()).tobytes() == np.float32(mx).tobytes()
     assert np.float32(gmn.item()).tobytes() == np.float32(mn).tobytes()
