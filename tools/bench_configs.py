@@ -131,7 +131,7 @@ def main():
     line("C2-int int64 max N=2^30", ms, n * 8)
     for thr in (1024, 384, 256):
         ms = timeit(lambda: runtime.reduce(x, mode="ordered", teams=sms, threads=thr, out=outf),
-                    10, 1)
+                    20, 5)
         line("C2 fp64 sum ORDERED (reference order, bit-exact) N=2^30", ms, n * 8,
              teams=sms, threads=thr)
 
