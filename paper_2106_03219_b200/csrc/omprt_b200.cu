@@ -157,7 +157,8 @@ int spmd_split(int teams) {
   if (g_variant == kNoSplit) return 1;
   const int sms = sm_count();
   if (sms <= 0 || teams * 2 > sms) return 1;
-  return sms / teams;
+  const int cl = sms / teams, cap = kMinPartialSlots / teams;  // teams * split partial slots
+  return cl < cap ? cl : cap;
 }
 
 // ORDERED row-group kernels (ordered.cuh).  Each CTA = nw streaming warps +
