@@ -26,7 +26,17 @@ runtime.dot(x, x, lb=5, ub=99_999, sched="static_chunked", chunk=40, teams=9, th
             mode="ordered")
 runtime.set_variant(20)
 runtime.reduce(x, sched="distribute", teams=8, threads=256, mode="ordered")
+# the literal walk's max/min team combine (left-biased tree, thread count not a multiple of 32)
+runtime.reduce(x, "max", sched="static", teams=5, threads=100, mode="ordered",
+               out=torch.full((1,), float("-inf"), dtype=torch.float64, device=dev))
 runtime.set_variant(0)
+# six-warp window policy (6 groups of 32 OpenMP threads per SM) for the sum and
+# the dot; max/min folders over full 256-partial batches as trees
+runtime.reduce(x, sched="distribute", teams=148, threads=192, mode="ordered")
+runtime.dot(x, x, sched="distribute", teams=148, threads=192, mode="ordered")
+runtime.reduce(xf, "min", sched="static", teams=148, threads=192, mode="ordered",
+               out=torch.full((1,), float("inf"), dtype=torch.float32, device=dev))
+runtime.axpy_minmax(0.5, xf, yf, sched="distribute", teams=148, threads=192, mode="ordered")
 # few-team SPMD launches split over CTAs (team_set_cta)
 runtime.reduce(xi, sched="static", teams=1, threads=128)
 runtime.reduce(x, sched="static_chunked", chunk=5, teams=3, threads=64)
