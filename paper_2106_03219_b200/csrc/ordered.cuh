@@ -475,12 +475,61 @@ template <class T> OMPRT_D T shfl_any(T v, int src_or_delta, bool down) {
 // so a full batch folds as a left-biased tree (each lane its 8 partials in
 // order, then lane i takes lane i+d for d = 1..16) with the sequential
 // fold's exact bits; a NaN cell value stays absorbing because acc is
-// combined last.  Sums fold strictly one by one.
+// combined first.  Sums fold strictly one by one.
 template <class T, class Combine>
 OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epoch, T acc,
                      T *ring, Combine &&comb) {
   constexpr int N = FoldLoad<T>::N;
   const uint32_t lane = threadIdx.x & 31u;
+  if constexpr (std::decay_t<Combine>::kAssoc) {
+    // Trees read only each lane's own 8 partials, so the batches stay in
+    // registers, four in flight: the fold is then bound by the partials'
+    // load latency / 4 instead of one load latency per batch.
+    const int64_t nfull = P / kFoldPer;
+    FoldLoad<T> R0, R1, R2, R3;
+    auto ld = [&](int64_t b, FoldLoad<T> &L) {
+      if (b < nfull) ord_folder_load<T>(tp, P, flags, epoch, b, L);
+    };
+    auto tree = [&](const FoldLoad<T> &L) {
+      T v = L.v[0];
+#pragma unroll
+      for (int k = 1; k < N; ++k) v = comb(v, L.v[k]);
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) v = comb(v, shfl_any<T>(v, d, true));
+      acc = comb(acc, shfl_any<T>(v, 0, false));
+    };
+    ld(0, R0);
+    ld(1, R1);
+    ld(2, R2);
+    ld(3, R3);
+    for (int64_t b = 0; b < nfull; b += 4) {
+      tree(R0);
+      ld(b + 4, R0);
+      if (b + 1 < nfull) {
+        tree(R1);
+        ld(b + 5, R1);
+      }
+      if (b + 2 < nfull) {
+        tree(R2);
+        ld(b + 6, R2);
+      }
+      if (b + 3 < nfull) {
+        tree(R3);
+        ld(b + 7, R3);
+      }
+    }
+    // the last, partial batch one by one (every lane folds the same values)
+    for (int64_t j = nfull * kFoldPer; j < P; ++j) {
+      if (j % 32 == 0 || j == nfull * kFoldPer)
+        while (ld_acquire_gpu(flags + j / 32) != epoch) {
+        }
+      acc = comb(acc, ld_cg(tp + j));
+    }
+    if (lane == 0)
+      trace_record(gridDim.x * ((blockDim.x >> 5) - 1), kTraceFolder,
+                   (uint32_t)((P + kFoldPer - 1) / kFoldPer), trace_t0());
+    return acc;
+  }
   const int64_t nb = (P + kFoldPer - 1) / kFoldPer;
   FoldLoad<T> L;
   ord_folder_load<T>(tp, P, flags, epoch, 0, L);
@@ -498,17 +547,8 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
     __syncwarp();
     const int64_t base = b * kFoldPer;
     if (base + kFoldPer <= P) {
-      if constexpr (std::decay_t<Combine>::kAssoc) {
-        T v = cur[lane * N];
-#pragma unroll
-        for (int k = 1; k < N; ++k) v = comb(v, cur[lane * N + k]);
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) v = comb(v, shfl_any<T>(v, d, true));
-        acc = comb(acc, shfl_any<T>(v, 0, false));
-      } else {
 #pragma unroll 32
-        for (int j = 0; j < kFoldPer; ++j) acc = comb(acc, cur[j]);
-      }
+      for (int j = 0; j < kFoldPer; ++j) acc = comb(acc, cur[j]);
     } else {
       for (int j = 0; base + j < P; ++j) acc = comb(acc, cur[j]);
     }
