@@ -483,12 +483,17 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
   const uint32_t lane = threadIdx.x & 31u;
   if constexpr (std::decay_t<Combine>::kAssoc) {
     // Trees read only each lane's own 8 partials, so the batches stay in
-    // registers, four in flight: the fold is then bound by the partials'
-    // load latency / 4 instead of one load latency per batch.
+    // registers.  Four batches (32 groups) per step: lane l acquires group
+    // l's ready flag, the warp barrier orders every lane's partial loads
+    // after all 32 acquires, then the 4 x 8 loads per lane go out together
+    // — one flag round trip and one load round trip per 1024 partials.
+    static_assert(kFoldPer == 8 * 32, "eight groups of 32 partials per batch");
     const int64_t nfull = P / kFoldPer;
     FoldLoad<T> R0, R1, R2, R3;
-    auto ld = [&](int64_t b, FoldLoad<T> &L) {
-      if (b < nfull) ord_folder_load<T>(tp, P, flags, epoch, b, L);
+    auto ldb = [&](int64_t b, FoldLoad<T> &L) {
+      const T *q = tp + b * kFoldPer + (int64_t)lane * N;
+#pragma unroll
+      for (int k = 0; k < N; ++k) L.v[k] = ld_cg(q + k);
     };
     auto tree = [&](const FoldLoad<T> &L) {
       T v = L.v[0];
@@ -498,25 +503,20 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
       for (int d = 1; d < 32; d <<= 1) v = comb(v, shfl_any<T>(v, d, true));
       acc = comb(acc, shfl_any<T>(v, 0, false));
     };
-    ld(0, R0);
-    ld(1, R1);
-    ld(2, R2);
-    ld(3, R3);
     for (int64_t b = 0; b < nfull; b += 4) {
+      const int64_t nbat = nfull - b < 4 ? nfull - b : 4;
+      if ((int64_t)lane < nbat * 8)
+        while (ld_acquire_gpu(flags + b * 8 + lane) != epoch) {
+        }
+      __syncwarp();
+      ldb(b, R0);
+      if (nbat > 1) ldb(b + 1, R1);
+      if (nbat > 2) ldb(b + 2, R2);
+      if (nbat > 3) ldb(b + 3, R3);
       tree(R0);
-      ld(b + 4, R0);
-      if (b + 1 < nfull) {
-        tree(R1);
-        ld(b + 5, R1);
-      }
-      if (b + 2 < nfull) {
-        tree(R2);
-        ld(b + 6, R2);
-      }
-      if (b + 3 < nfull) {
-        tree(R3);
-        ld(b + 7, R3);
-      }
+      if (nbat > 1) tree(R1);
+      if (nbat > 2) tree(R2);
+      if (nbat > 3) tree(R3);
     }
     // the last, partial batch one by one (every lane folds the same values)
     for (int64_t j = nfull * kFoldPer; j < P; ++j) {
