@@ -125,8 +125,15 @@ const char *omprt_version(void);
 /* Message of the last failing call on this host thread ("" if none). */
 const char *omprt_last_error(void);
 
-/* Select the CUDA device for this host thread and clear its trap word. */
+/* Clear the trap word of CUDA device `device`.  The calling thread's current
+ * device is left unchanged: every stream-taking entry point below runs on
+ * its stream's device (cudaStreamGetDevice), restoring the caller's current
+ * device on return; with a NULL (legacy default) stream it runs on the
+ * current device. */
 int omprt_device_init(int device);
+
+/* Tuning knobs are per host thread (a tuning call never changes the kernel
+ * another thread's launch selects). */
 
 /* Tuning knob (not part of the reference interface): 16-byte vectors each
  * lane keeps in flight per loop iteration in the LDG-fed SPMD loops (2, 4 or
@@ -358,11 +365,37 @@ int omprt_fill(void *d_x, int64_t n, int dtype, uint64_t seed, int k, int64_t of
  * (host.py:255-296): copy-in of h_x (n elements; pinned or pageable host
  * memory) to a device buffer, omprt_reduce over [0, n-1], copy-out of the
  * scalar result into *h_out (which holds the initial value on entry), only on
- * status 0.  Synchronous.  The device buffers are cached across calls. */
+ * status 0.  Synchronous.  The device buffers are cached across calls, per
+ * CUDA device (the calling thread's current device runs the region). */
 int omprt_reduce_host(const void *h_x, int64_t n, int dtype, int op, int sched,
                       int64_t chunk, int teams, int threads, int mode, void *h_out);
 
-/* Release the buffers cached by omprt_reduce_host. */
+/* Host-buffer offload of the config-3 region (axpy + max/min): copy-in of
+ * h_x and h_y (n floats each), omprt_axpy_minmax over [0, n-1], copy-out of
+ * y (tofrom) and the two cells *h_max / *h_min (which hold the initial
+ * values on entry) — only on status 0 (host.py:293-295).  Synchronous. */
+int omprt_axpy_minmax_host(float a, const float *h_x, float *h_y, int64_t n, int sched,
+                           int64_t chunk, int teams, int threads, int mode, float *h_max,
+                           float *h_min);
+
+/* Host-buffer offload of the fp64 dot product: copy-in of h_x, h_y,
+ * omprt_dot over [0, n-1], copy-out of *h_out only on status 0. */
+int omprt_dot_host(const double *h_x, const double *h_y, int64_t n, int sched, int64_t chunk,
+                   int teams, int threads, int mode, double *h_out);
+
+/* Host-buffer offload of the generic-mode region (omprt_generic_reduce over
+ * [0, n-1]): copy-in, launch, synchronise, and on a device trap return
+ * OMPRT_TRAP with *h_out and h_team_offsets untouched (the trap word stays
+ * set for omprt_check_trap: tgt_target's status 2, host.py:289-292);
+ * otherwise copy-out of the cell and, when h_team_offsets is not NULL, the
+ * `teams` arena offsets. */
+int omprt_generic_reduce_host(const void *h_x, int64_t n, int dtype, int op, int teams,
+                              int par_threads, int ordered, int64_t pad_bytes, int heap_fallback,
+                              int64_t heap_bytes_per_team, void *h_out,
+                              int64_t *h_team_offsets);
+
+/* Release the device staging cached by the host-buffer entries (on every
+ * device that has any: the staging is kept per CUDA device). */
 int omprt_release_host_cache(void);
 
 /* ========================================================================= */

@@ -72,6 +72,8 @@ def lib():
                                  C.POINTER(C.c_double)]
         L.oracle_accurate_dot_gen.argtypes = [u64, i64, i64]
         L.oracle_accurate_dot_gen.restype = C.c_double
+        L.oracle_exact_dot_gen.argtypes = [u64, i64, i64]
+        L.oracle_exact_dot_gen.restype = C.c_double
         L.oracle_generic_reduce.argtypes = [vp, u64, C.c_int, i64, i64, C.c_int, C.c_int, i64,
                                             i64, vp]
         L.oracle_arena_replay.argtypes = [vp, C.c_int, C.c_int, i64, C.c_int, i64, C.c_int, vp]
@@ -177,6 +179,11 @@ def dot(x, y, lb: int, ub: int, sched: int, chunk: int, teams: int, threads: int
 
 def accurate_dot_gen(lb: int, ub: int, *, seed: int = SEED) -> float:
     return lib().oracle_accurate_dot_gen(seed, lb, ub)
+
+
+def exact_dot_gen(lb: int, ub: int, *, seed: int = SEED) -> float:
+    """The generated dot accumulated exactly in 128-bit integer halves."""
+    return lib().oracle_exact_dot_gen(seed, lb, ub)
 
 
 def generic_reduce(x, lb: int, ub: int, dtype: int, op: int, teams: int, P: int, init=0, *,

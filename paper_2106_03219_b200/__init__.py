@@ -31,6 +31,9 @@ from .offload import (
     RegionKernel,
     TargetCall,
     TrapKind,
+    axpy_minmax_host,
+    dot_host,
+    generic_reduce_host,
     kernel_name,
     reduce_host,
     tgt_target,
@@ -48,6 +51,9 @@ __all__ = [
     "TRAP_CODES",
     "TargetCall",
     "TrapKind",
+    "axpy_minmax_host",
+    "dot_host",
+    "generic_reduce_host",
     "kernel_name",
     "load",
     "reduce_host",

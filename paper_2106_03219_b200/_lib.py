@@ -103,6 +103,14 @@ _SIGS = {
                    C.c_int),
     "omprt_reduce_host": ([C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int,
                            C.c_int, C.c_int, C.c_void_p], C.c_int),
+    "omprt_axpy_minmax_host": ([C.c_float, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
+                                C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p],
+                               C.c_int),
+    "omprt_dot_host": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int64, C.c_int, C.c_int,
+                        C.c_int, C.c_void_p], C.c_int),
+    "omprt_generic_reduce_host": ([C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_int, C.c_int64, C.c_int, C.c_int64, C.c_void_p,
+                                   C.c_void_p], C.c_int),
     "omprt_release_host_cache": ([], C.c_int),
     "omprt_image_load": ([C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)], C.c_int),
     "omprt_image_unload": ([C.c_void_p], C.c_int),

@@ -49,8 +49,39 @@ int check_launch(const char *what) {
 
 inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-int g_unroll = 4;   // tuning knob: vectors in flight per lane per iteration
-int g_variant = 0;  // tuning knob: kernel variant of the fp64 sum (0 = default)
+// Every stream-taking entry point runs on the stream's device: the launches,
+// the SM count, the dynamic-smem opt-in and the trap word all follow the
+// calling thread's current device, so a caller holding streams of several
+// devices (one process driving two GPUs) must not have to select the device
+// first.  The previous current device is restored on return.  The legacy /
+// per-thread default streams (handles 0, 1, 2) keep the current device.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(void *stream) {
+    if (reinterpret_cast<uintptr_t>(stream) <= 2) return;
+    int want = -1, cur = -1;
+    if (cudaStreamGetDevice(S(stream), &want) != cudaSuccess) {
+      cudaGetLastError();  // an invalid handle surfaces at the launch instead
+      return;
+    }
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != want && cudaSetDevice(want) == cudaSuccess)
+      prev_ = cur;
+  }
+  ~DeviceGuard() {
+    if (prev_ >= 0) cudaSetDevice(prev_);
+  }
+  DeviceGuard(const DeviceGuard &) = delete;
+  DeviceGuard &operator=(const DeviceGuard &) = delete;
+
+ private:
+  int prev_ = -1;
+};
+#define OMPRT_ON_STREAM_DEVICE(stream) DeviceGuard device_guard_(stream)
+
+// Tuning knobs are per host thread: a tuning call in one thread never
+// changes the kernel another caller's launch selects.
+thread_local int g_unroll = 4;   // vectors in flight per lane per iteration
+thread_local int g_variant = 0;  // kernel variant of the fp64 sum (0 = default)
 constexpr int kOrderedLiteral = 20;  // variant: ORDERED mode through the literal walk
 bool g_trace_on = false;  // a trace ring is installed (selects traced kernel instances)
 
@@ -528,14 +559,53 @@ int launch_generic_op(int op, const void *x, int64_t lb, int64_t ub, int teams, 
 
 size_t generic_ws_core(int teams) { return ws_bytes(teams, 0, OMPRT_MODE_SPMD, 1); }
 
-// host-buffer entry cache
+// Host-buffer (tgt_target-shaped) entries: device staging cached per CUDA
+// device (a buffer belongs to the context it was allocated in, so a caller
+// that switches devices gets that device's own staging, never another's).
+struct HostStaging {
+  void *buf[2] = {nullptr, nullptr};  // input / in-out arrays
+  size_t bytes[2] = {0, 0};
+  void *ws = nullptr;                 // zeroed construct workspace
+  size_t ws_bytes = 0;
+  void *cells = nullptr;              // 64 bytes: result cells + team offsets spill
+  int64_t *offs = nullptr;            // generic mode: per-team arena offsets
+  size_t offs_bytes = 0;
+  cudaStream_t stream = nullptr;
+};
 std::mutex g_host_mu;
-void *g_host_x = nullptr;
-size_t g_host_x_bytes = 0;
-void *g_host_ws = nullptr;
-size_t g_host_ws_bytes = 0;
-void *g_host_out = nullptr;
-cudaStream_t g_host_stream = nullptr;
+std::unordered_map<int, HostStaging> g_host;
+
+int staging_grow(void *&p, size_t &have, size_t want, bool zero) {
+  if (want <= have) return OMPRT_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  have = 0;
+  if (cudaMalloc(&p, want) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(OMPRT_ENOMEM, "host entry: cannot allocate %zu device bytes", want);
+  }
+  if (zero && cudaMemset(p, 0, want) != cudaSuccess)
+    return fail(OMPRT_ECUDA, "host entry: cannot zero the workspace");
+  have = want;
+  return OMPRT_OK;
+}
+
+// The calling thread's device's staging, with room for two arrays of
+// (b0, b1) bytes and a workspace of ws bytes.  g_host_mu must be held.
+int staging(HostStaging *&out, size_t b0, size_t b1, size_t ws) {
+  int dev = 0;
+  OMPRT_CUDA(cudaGetDevice(&dev));
+  HostStaging &h = g_host[dev];
+  if (!h.stream) OMPRT_CUDA(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+  int rc;
+  if ((rc = staging_grow(h.buf[0], h.bytes[0], b0, false)) ||
+      (rc = staging_grow(h.buf[1], h.bytes[1], b1, false)) ||
+      (rc = staging_grow(h.ws, h.ws_bytes, ws, true)))
+    return rc;
+  if (!h.cells) OMPRT_CUDA(cudaMalloc(&h.cells, 64));
+  out = &h;
+  return OMPRT_OK;
+}
 
 }  // namespace
 
@@ -548,9 +618,13 @@ const char *omprt_version(void) { return "omprt_b200 0.1.0 sm_100a"; }
 const char *omprt_last_error(void) { return t_last_error.c_str(); }
 
 int omprt_device_init(int device) {
+  int prev = -1;
+  OMPRT_CUDA(cudaGetDevice(&prev));
   OMPRT_CUDA(cudaSetDevice(device));
   TrapWord z = {0, 0, 0, 0};
-  OMPRT_CUDA(cudaMemcpyToSymbol(g_trap, &z, sizeof(z)));
+  const cudaError_t e = cudaMemcpyToSymbol(g_trap, &z, sizeof(z));
+  if (prev != device) cudaSetDevice(prev);  // the caller's current device is left alone
+  if (e != cudaSuccess) return fail(OMPRT_ECUDA, "device_init: %s", cudaGetErrorString(e));
   return OMPRT_OK;
 }
 
@@ -583,6 +657,7 @@ int nccl_dtype(int dtype, int op) {
 
 int omprt_allreduce(void *d_buf, int64_t count, int dtype, int op, void *nccl_comm,
                     void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   if (count < 0 || (count > 0 && !d_buf) || !nccl_comm)
     return fail(OMPRT_EINVAL, "allreduce: bad arguments");
   const int nt = nccl_dtype(dtype, op);
@@ -651,6 +726,7 @@ int omprt_reduce_exchange(const void *d_x, int64_t lb, int64_t ub, int dtype, in
                           int64_t chunk, int teams, int threads, void *d_ws, void *d_out,
                           const void *d_peers, int rank, int world, uint64_t key, uint64_t step,
                           void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
   if (!d_ws || !d_out || !d_peers || (!d_x && ub >= lb) || world < 1 || rank < 0 ||
@@ -690,6 +766,7 @@ int omprt_num_sms(void) {
 }
 
 int omprt_check_trap(void *stream, int *kind, int *code, int *team, int *thread) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   OMPRT_CUDA(cudaStreamSynchronize(S(stream)));
   TrapWord t;
   OMPRT_CUDA(cudaMemcpyFromSymbol(&t, g_trap, sizeof(t)));
@@ -731,6 +808,7 @@ int omprt_static_bounds(int64_t lb, int64_t ub, int64_t tid, int64_t nthreads, i
 
 int omprt_bounds_dump(int64_t lb, int64_t ub, int sched, int64_t chunk, int teams, int threads,
                       int64_t *d_out, void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
   if (!d_out) return fail(OMPRT_EINVAL, "bounds_dump: null output");
@@ -746,6 +824,7 @@ size_t omprt_reduce_workspace_bytes(int teams, int threads, int mode) {
 int omprt_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int sched,
                  int64_t chunk, int teams, int threads, int mode, void *d_ws, void *d_out,
                  void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
   if (!d_ws || !d_out || (!d_x && ub >= lb))
@@ -779,6 +858,7 @@ int launch_axpy_spmd(float a, const float *d_x, float *d_y, LoopArgs la, int tea
 int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t ub, int sched,
                       int64_t chunk, int teams, int threads, int mode, void *d_ws, float *d_max,
                       float *d_min, void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
   if (!d_ws || !d_max || !d_min || ((!d_x || !d_y) && ub >= lb))
@@ -825,6 +905,7 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
 int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int sched,
               int64_t chunk, int teams, int threads, int mode, void *d_ws, double *d_out,
               void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
   if (!d_ws || !d_out || ((!d_x || !d_y) && ub >= lb))
@@ -888,6 +969,7 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
 
 int omprt_combine_partials(const void *d_partials, int count, int dtype, int op, void *d_out,
                            void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   if (count < 0 || !d_out || (count > 0 && !d_partials))
     return fail(OMPRT_EINVAL, "combine_partials: bad arguments");
   return by_dtype<CombineF>(dtype, op, d_partials, count, d_out, S(stream));
@@ -905,6 +987,7 @@ int omprt_generic_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int
                          int par_threads, int ordered, int64_t pad_bytes, int heap_fallback,
                          int64_t heap_bytes_per_team, void *d_ws, void *d_out,
                          int64_t *d_team_offsets, void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   if (teams < 1) return fail(OMPRT_EINVAL, "teams must be >= 1");
   if (par_threads < 32 || par_threads % 32 != 0 || par_threads + 32 > kMaxThreads)
     return fail(OMPRT_EINVAL, "par_threads must be a multiple of 32 in 32..%d (got %d)",
@@ -937,6 +1020,7 @@ int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads
                        int caller_tid, int64_t capacity, int heap_fallback,
                        int64_t heap_bytes_per_team, void *d_heap, int check_uninit,
                        int64_t *d_results, void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads))) return rc;
   if (nops < 0 || (nops > 0 && (!d_script || !d_results)))
@@ -970,6 +1054,7 @@ int omprt_arena_replay(const int64_t *d_script, int nops, int teams, int threads
 
 int omprt_atomic_probe(int kind, int dtype, const uint64_t *d_operands, const uint64_t *d_desired,
                        uint64_t *d_cell, uint64_t *d_old, int teams, int threads, void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads))) return rc;
   if ((rc = check_atomic(kind, dtype, d_desired))) return rc;
@@ -992,6 +1077,7 @@ int omprt_atomic_probe(int kind, int dtype, const uint64_t *d_operands, const ui
 
 int omprt_atomic_apply(int kind, int dtype, uint64_t *d_cells, const uint64_t *d_operands,
                        const uint64_t *d_desired, uint64_t *d_old, int64_t n, void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_atomic(kind, dtype, d_desired))) return rc;
   if (n < 0 || (n > 0 && (!d_cells || !d_operands || !d_old)))
@@ -1012,6 +1098,7 @@ int omprt_atomic_program(const int32_t *d_kinds, const uint64_t *d_operands,
                          const uint64_t *d_desired, const int64_t *d_offsets, int64_t nops,
                          int dtype, uint64_t *d_cell, uint64_t *d_old, int teams, int threads,
                          void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   int rc;
   if ((rc = check_grid(teams, threads))) return rc;
   if (dtype != OMPRT_I32 && dtype != OMPRT_U32 && dtype != OMPRT_I64 && dtype != OMPRT_U64)
@@ -1038,6 +1125,7 @@ int omprt_atomic_program(const int32_t *d_kinds, const uint64_t *d_operands,
 
 int omprt_fill(void *d_x, int64_t n, int dtype, uint64_t seed, int k, int64_t offset,
                void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   if (n < 0 || (n > 0 && !d_x)) return fail(OMPRT_EINVAL, "fill: bad arguments");
   return by_dtype<FillF>(dtype, d_x, n, seed, k, offset, S(stream));
 }
@@ -1050,49 +1138,142 @@ int omprt_reduce_host(const void *h_x, int64_t n, int dtype, int op, int sched, 
   if (n < 0 || !h_out || (n > 0 && !h_x)) return fail(OMPRT_EINVAL, "reduce_host: bad arguments");
   int rc;
   if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
-  if (!g_host_stream) OMPRT_CUDA(cudaStreamCreateWithFlags(&g_host_stream, cudaStreamNonBlocking));
   const size_t xbytes = (size_t)n * es;
-  if (xbytes > g_host_x_bytes) {
-    if (g_host_x) cudaFree(g_host_x);
-    g_host_x = nullptr;
-    g_host_x_bytes = 0;
-    if (cudaMalloc(&g_host_x, xbytes) != cudaSuccess)
-      return fail(OMPRT_ENOMEM, "reduce_host: cannot allocate %zu device bytes", xbytes);
-    g_host_x_bytes = xbytes;
-  }
-  const size_t wsb = omprt_reduce_workspace_bytes(teams, threads, mode);
-  if (wsb > g_host_ws_bytes) {
-    if (g_host_ws) cudaFree(g_host_ws);
-    g_host_ws = nullptr;
-    g_host_ws_bytes = 0;
-    if (cudaMalloc(&g_host_ws, wsb) != cudaSuccess)
-      return fail(OMPRT_ENOMEM, "reduce_host: cannot allocate workspace");
-    OMPRT_CUDA(cudaMemset(g_host_ws, 0, wsb));
-    g_host_ws_bytes = wsb;
-  }
-  if (!g_host_out) OMPRT_CUDA(cudaMalloc(&g_host_out, 16));
-  cudaStream_t st = g_host_stream;
+  HostStaging *h = nullptr;
+  if ((rc = staging(h, xbytes, 0, omprt_reduce_workspace_bytes(teams, threads, mode)))) return rc;
+  cudaStream_t st = h->stream;
   // copy-in (tgt_target host.py:276-281)
-  if (xbytes) OMPRT_CUDA(cudaMemcpyAsync(g_host_x, h_x, xbytes, cudaMemcpyHostToDevice, st));
-  OMPRT_CUDA(cudaMemcpyAsync(g_host_out, h_out, es, cudaMemcpyHostToDevice, st));
-  rc = omprt_reduce(g_host_x, 0, n - 1, dtype, op, sched, chunk, teams, threads, mode, g_host_ws,
-                    g_host_out, st);
+  if (xbytes) OMPRT_CUDA(cudaMemcpyAsync(h->buf[0], h_x, xbytes, cudaMemcpyHostToDevice, st));
+  OMPRT_CUDA(cudaMemcpyAsync(h->cells, h_out, es, cudaMemcpyHostToDevice, st));
+  rc = omprt_reduce(h->buf[0], 0, n - 1, dtype, op, sched, chunk, teams, threads, mode, h->ws,
+                    h->cells, st);
   if (rc) return rc;
   // copy-out only on status 0 (host.py:293-295)
   unsigned char res[16];
-  OMPRT_CUDA(cudaMemcpyAsync(res, g_host_out, es, cudaMemcpyDeviceToHost, st));
+  OMPRT_CUDA(cudaMemcpyAsync(res, h->cells, es, cudaMemcpyDeviceToHost, st));
   OMPRT_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(h_out, res, es);
+  return OMPRT_OK;
+}
+
+int omprt_axpy_minmax_host(float a, const float *h_x, float *h_y, int64_t n, int sched,
+                           int64_t chunk, int teams, int threads, int mode, float *h_max,
+                           float *h_min) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  if (n < 0 || !h_max || !h_min || (n > 0 && (!h_x || !h_y)))
+    return fail(OMPRT_EINVAL, "axpy_minmax_host: bad arguments");
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  const size_t bytes = (size_t)n * sizeof(float);
+  HostStaging *h = nullptr;
+  if ((rc = staging(h, bytes, bytes, omprt_reduce_workspace_bytes(teams, threads, mode))))
+    return rc;
+  cudaStream_t st = h->stream;
+  float *cells = static_cast<float *>(h->cells);
+  const float init[2] = {*h_max, *h_min};
+  if (bytes) {
+    OMPRT_CUDA(cudaMemcpyAsync(h->buf[0], h_x, bytes, cudaMemcpyHostToDevice, st));
+    OMPRT_CUDA(cudaMemcpyAsync(h->buf[1], h_y, bytes, cudaMemcpyHostToDevice, st));
+  }
+  OMPRT_CUDA(cudaMemcpyAsync(cells, init, sizeof init, cudaMemcpyHostToDevice, st));
+  rc = omprt_axpy_minmax(a, static_cast<const float *>(h->buf[0]), static_cast<float *>(h->buf[1]),
+                         0, n - 1, sched, chunk, teams, threads, mode, h->ws, cells, cells + 1, st);
+  if (rc) return rc;
+  // y is tofrom: back to the caller with the two cells, only on status 0
+  float res[2];
+  if (bytes) OMPRT_CUDA(cudaMemcpyAsync(h_y, h->buf[1], bytes, cudaMemcpyDeviceToHost, st));
+  OMPRT_CUDA(cudaMemcpyAsync(res, cells, sizeof res, cudaMemcpyDeviceToHost, st));
+  OMPRT_CUDA(cudaStreamSynchronize(st));
+  *h_max = res[0];
+  *h_min = res[1];
+  return OMPRT_OK;
+}
+
+int omprt_dot_host(const double *h_x, const double *h_y, int64_t n, int sched, int64_t chunk,
+                   int teams, int threads, int mode, double *h_out) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  if (n < 0 || !h_out || (n > 0 && (!h_x || !h_y)))
+    return fail(OMPRT_EINVAL, "dot_host: bad arguments");
+  int rc;
+  if ((rc = check_grid(teams, threads)) || (rc = check_sched(sched, chunk))) return rc;
+  const size_t bytes = (size_t)n * sizeof(double);
+  HostStaging *h = nullptr;
+  if ((rc = staging(h, bytes, bytes, omprt_reduce_workspace_bytes(teams, threads, mode))))
+    return rc;
+  cudaStream_t st = h->stream;
+  double *cell = static_cast<double *>(h->cells);
+  if (bytes) {
+    OMPRT_CUDA(cudaMemcpyAsync(h->buf[0], h_x, bytes, cudaMemcpyHostToDevice, st));
+    OMPRT_CUDA(cudaMemcpyAsync(h->buf[1], h_y, bytes, cudaMemcpyHostToDevice, st));
+  }
+  OMPRT_CUDA(cudaMemcpyAsync(cell, h_out, sizeof(double), cudaMemcpyHostToDevice, st));
+  rc = omprt_dot(static_cast<const double *>(h->buf[0]), static_cast<const double *>(h->buf[1]),
+                 0, n - 1, sched, chunk, teams, threads, mode, h->ws, cell, st);
+  if (rc) return rc;
+  double res;
+  OMPRT_CUDA(cudaMemcpyAsync(&res, cell, sizeof res, cudaMemcpyDeviceToHost, st));
+  OMPRT_CUDA(cudaStreamSynchronize(st));
+  *h_out = res;
+  return OMPRT_OK;
+}
+
+int omprt_generic_reduce_host(const void *h_x, int64_t n, int dtype, int op, int teams,
+                              int par_threads, int ordered, int64_t pad_bytes, int heap_fallback,
+                              int64_t heap_bytes_per_team, void *h_out,
+                              int64_t *h_team_offsets) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  const size_t es = dtype_size(dtype);
+  if (!es) return fail(OMPRT_EINVAL, "unknown dtype %d", dtype);
+  if (n < 0 || !h_out || (n > 0 && !h_x) || teams < 1)
+    return fail(OMPRT_EINVAL, "generic_reduce_host: bad arguments");
+  int rc;
+  const size_t xbytes = (size_t)n * es;
+  HostStaging *h = nullptr;
+  if ((rc = staging(h, xbytes, 0,
+                    omprt_generic_workspace_bytes(teams, par_threads, heap_fallback,
+                                                  heap_bytes_per_team))))
+    return rc;
+  if (h_team_offsets &&
+      (rc = staging_grow(reinterpret_cast<void *&>(h->offs), h->offs_bytes,
+                         (size_t)teams * sizeof(int64_t), false)))
+    return rc;
+  cudaStream_t st = h->stream;
+  if (xbytes) OMPRT_CUDA(cudaMemcpyAsync(h->buf[0], h_x, xbytes, cudaMemcpyHostToDevice, st));
+  OMPRT_CUDA(cudaMemcpyAsync(h->cells, h_out, es, cudaMemcpyHostToDevice, st));
+  rc = omprt_generic_reduce(h->buf[0], 0, n - 1, dtype, op, teams, par_threads, ordered,
+                            pad_bytes, heap_fallback, heap_bytes_per_team, h->ws, h->cells,
+                            h_team_offsets ? h->offs : nullptr, st);
+  if (rc) return rc;
+  // a device trap (arena overflow, non-LIFO free, ...) is status 2 with the
+  // caller's buffers untouched (host.py:289-295); the trap word stays set
+  // for omprt_check_trap
+  OMPRT_CUDA(cudaStreamSynchronize(st));
+  TrapWord t;
+  OMPRT_CUDA(cudaMemcpyFromSymbol(&t, g_trap, sizeof(t)));
+  if (t.kind) return fail(OMPRT_TRAP, "generic_reduce_host: device trap kind %d code %d", t.kind,
+                          t.code);
+  unsigned char res[16];
+  OMPRT_CUDA(cudaMemcpy(res, h->cells, es, cudaMemcpyDeviceToHost));
+  if (h_team_offsets)
+    OMPRT_CUDA(cudaMemcpy(h_team_offsets, h->offs, (size_t)teams * sizeof(int64_t),
+                          cudaMemcpyDeviceToHost));
   std::memcpy(h_out, res, es);
   return OMPRT_OK;
 }
 
 int omprt_release_host_cache(void) {
   std::lock_guard<std::mutex> lk(g_host_mu);
-  if (g_host_x) cudaFree(g_host_x);
-  if (g_host_ws) cudaFree(g_host_ws);
-  if (g_host_out) cudaFree(g_host_out);
-  g_host_x = g_host_ws = g_host_out = nullptr;
-  g_host_x_bytes = g_host_ws_bytes = 0;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (auto &kv : g_host) {
+    HostStaging &h = kv.second;
+    cudaSetDevice(kv.first);
+    for (void *p : {h.buf[0], h.buf[1], h.ws, h.cells, static_cast<void *>(h.offs)})
+      if (p) cudaFree(p);
+    if (h.stream) cudaStreamDestroy(h.stream);
+  }
+  g_host.clear();
+  if (prev >= 0) cudaSetDevice(prev);
   return OMPRT_OK;
 }
 
@@ -1114,6 +1295,7 @@ int omprt_image_unload(void *handle) {
 
 int omprt_image_launch(void *handle, const char *kernel, int teams, int threads,
                        size_t shared_bytes, const void *argv, size_t argv_bytes, void *stream) {
+  OMPRT_ON_STREAM_DEVICE(stream);
   if (!handle || !kernel || !argv || !argv_bytes)
     return fail(OMPRT_EINVAL, "image_launch: bad arguments");
   // GridConfig limits (vgpu.py:50-61)

@@ -207,15 +207,77 @@ RT_D u64 rt_rmw_value(u32 kind, bool sgn, int bits, u64 old, u64 e, u64 d) {
   }
 }
 
+// 128-bit compare-and-swap (atom.cas.b128, sm_90+; generic address: global
+// or shared).  Returns the previous 16 bytes.
+RT_D unsigned __int128 rt_cas128(void *a, unsigned __int128 e, unsigned __int128 d) {
+  u64 olo, ohi;
+  asm volatile(
+      "{\n\t.reg .b128 e, d, o;\n\t"
+      "mov.b128 e, {%2, %3};\n\t"
+      "mov.b128 d, {%4, %5};\n\t"
+      "atom.cas.b128 o, [%6], e, d;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(olo), "=l"(ohi)
+      : "l"((u64)e), "l"((u64)(e >> 64)), "l"((u64)d), "l"((u64)(d >> 64)), "l"(a)
+      : "memory");
+  return ((unsigned __int128)ohi << 64) | olo;
+}
+
+// A cell that is not naturally aligned (the vgpu's RMW is atomic at any byte
+// offset, vgpu.py:586-625): compare-and-swap loop on the enclosing aligned
+// 8-byte word, or 16-byte line (atom.cas.b128) when the cell straddles two
+// words; a cell straddling a 16-byte line cannot be updated by one hardware
+// RMW and traps Abort instead of losing updates.
+__device__ __noinline__ u64 rt_atomic_unaligned(const P &p, u32 kind, bool sgn, u32 w, u64 e,
+                                                u64 d, u32 site) {
+  const int bits = (int)w * 8;
+  const u64 m = bits == 32 ? 0xffffffffull : ~0ull;
+  const unsigned long long addr = (unsigned long long)p.p;
+  if ((addr & 7) + w <= 8) {
+    unsigned long long *word = (unsigned long long *)(addr & ~7ull);
+    const int sh = (int)(addr & 7) * 8;
+    unsigned long long cur = *(volatile unsigned long long *)word;
+    for (;;) {
+      const u64 old = (cur >> sh) & m;
+      const u64 nv = rt_rmw_value(kind, sgn, bits, old, e, d) & m;
+      const unsigned long long nxt = (cur & ~(m << sh)) | (nv << sh);
+      const unsigned long long prev = atomicCAS(word, cur, nxt);
+      if (prev == cur) return old;
+      cur = prev;
+    }
+  }
+  if ((addr & 15) + w <= 16) {
+    void *line = (void *)(addr & ~15ull);
+    const int sh = (int)(addr & 15) * 8;
+    const unsigned __int128 mm = (unsigned __int128)m << sh;
+    unsigned __int128 cur = ((unsigned __int128)((volatile u64 *)line)[1] << 64) |
+                            ((volatile u64 *)line)[0];
+    for (;;) {
+      const u64 old = (u64)(cur >> sh) & m;
+      const u64 nv = rt_rmw_value(kind, sgn, bits, old, e, d) & m;
+      const unsigned __int128 nxt = (cur & ~mm) | ((unsigned __int128)nv << sh);
+      const unsigned __int128 prev = rt_cas128(line, cur, nxt);
+      if (prev == cur) return old;
+      cur = prev;
+    }
+  }
+  rt_trap(RT_ABORT, site, w, rt_off(p), 0, rt_label(p));
+  return 0;
+}
+
 __device__ __noinline__ u64 rt_atomic(const P &p, u32 kind, bool sgn, u32 w, u64 e, u64 d,
                                       u32 site_ld, u32 site_st) {
   rt_check(p, w, site_ld);
   if (p.p + w > p.hi) rt_trap(RT_OUT_OF_BOUNDS, site_st, w, rt_off(p), 0, rt_label(p));
   const int bits = (int)w * 8;
   u64 old;
-  if (p.space == RT_SLOT || ((unsigned long long)p.p & (w - 1)) != 0) {
+  if (p.space == RT_SLOT) {
     old = rt_raw_ld(p, w);
     rt_raw_st(p, w, rt_rmw_value(kind, sgn, bits, old, e, d));
+  } else if (((unsigned long long)p.p & (w - 1)) != 0) {
+    __threadfence();
+    old = rt_atomic_unaligned(p, kind, sgn, w, e, d, site_st);
+    __threadfence();
   } else {
     __threadfence();
     if (w == 4) {

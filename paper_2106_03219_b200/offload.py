@@ -251,6 +251,15 @@ def tgt_target(call: TargetCall, bundle, device="b200", force_fail: bool = False
         tracer.__enter__()
     try:
         _launch_construct(rk, c, r, scal, dbufs, teams, threads, dev)
+    except IndexError as err:
+        # the loop would index a buffer outside its extent: the vgpu traps
+        # OutOfBounds on that access (vgpu.py:28-36) -> status 2, the
+        # caller's buffers untouched, nothing launched
+        if out is not None:
+            out["result"] = {"construct": c, "teams": teams, "threads": threads}
+            out["trace"] = []
+            out["trap"] = (TrapKind.OUT_OF_BOUNDS.value, str(err))
+        return 2
     finally:
         if tracer is not None:
             tracer.__exit__(None, None, None)
@@ -350,3 +359,84 @@ def reduce_host(x: np.ndarray | torch.Tensor, cell, *, op="add", sched="static",
         _lib.SCHED_NAMES[sched] if isinstance(sched, str) else sched, chunk, teams, threads,
         _lib.MODE_NAMES[mode] if isinstance(mode, str) else mode, C.c_void_p(cp)),
         "omprt_reduce_host")
+
+
+def _host_ptr(a, what: str):
+    """(address, numel, dtype code) of a host array / CPU tensor."""
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            raise TypeError(f"{what} takes host memory")
+        if not a.is_contiguous():
+            raise ValueError(f"{what}: host tensors must be contiguous")
+        return a.data_ptr(), a.numel(), runtime.dtype_code(a.dtype)
+    a = np.asarray(a)
+    if not a.flags.c_contiguous:
+        raise ValueError(f"{what}: host arrays must be contiguous")
+    return a.ctypes.data, a.size, runtime.dtype_code(torch.from_numpy(a[:0]).dtype)
+
+
+def _code(table: dict, v) -> int:
+    return table[v] if isinstance(v, str) else v
+
+
+def axpy_minmax_host(a: float, x, y, cells, *, sched="distribute_chunked", chunk: int = 1,
+                     teams: int, threads: int, mode="spmd") -> None:
+    """omprt_axpy_minmax_host: copy-in of x and y, the fused axpy + max/min
+    construct, copy-out of y and cells = [max, min] (host fp32 arrays holding
+    the initial values) — only on status 0 (host.py:293-295)."""
+    xp, n, dx = _host_ptr(x, "axpy_minmax_host")
+    yp, ny, dy = _host_ptr(y, "axpy_minmax_host")
+    cp, nc, dc = _host_ptr(cells, "axpy_minmax_host")
+    if (dx, dy, dc) != (_lib.F32,) * 3 or ny < n or nc < 2:
+        raise TypeError("axpy_minmax_host takes fp32 x, y (len(y) >= len(x)) and 2 cells")
+    _lib.ensure_device(torch.cuda.current_device())
+    f = C.POINTER(C.c_float)
+    _lib.check(_lib.load().omprt_axpy_minmax_host(
+        C.c_float(a), C.c_void_p(xp), C.c_void_p(yp), n, _code(_lib.SCHED_NAMES, sched), chunk,
+        teams, threads, _code(_lib.MODE_NAMES, mode), C.cast(C.c_void_p(cp), f),
+        C.cast(C.c_void_p(cp + 4), f)), "omprt_axpy_minmax_host")
+
+
+def dot_host(x, y, cell, *, sched="static", chunk: int = 1, teams: int, threads: int,
+             mode="spmd") -> None:
+    """omprt_dot_host: copy-in of x and y, the fp64 dot construct, copy-out of
+    the cell (a 1-element host fp64 array holding the initial value)."""
+    xp, n, dx = _host_ptr(x, "dot_host")
+    yp, ny, dy = _host_ptr(y, "dot_host")
+    cp, _, dc = _host_ptr(cell, "dot_host")
+    if (dx, dy, dc) != (_lib.F64,) * 3 or ny < n:
+        raise TypeError("dot_host takes fp64 x, y (len(y) >= len(x)) and an fp64 cell")
+    _lib.ensure_device(torch.cuda.current_device())
+    _lib.check(_lib.load().omprt_dot_host(
+        C.c_void_p(xp), C.c_void_p(yp), n, _code(_lib.SCHED_NAMES, sched), chunk, teams, threads,
+        _code(_lib.MODE_NAMES, mode), C.c_void_p(cp)), "omprt_dot_host")
+
+
+def generic_reduce_host(x, cell, *, op="add", teams: int = 1024, par_threads: int = 256,
+                        ordered: bool = False, pad_bytes: int = 0, heap_fallback: bool = False,
+                        heap_bytes_per_team: int = 1 << 20, team_offsets=None,
+                        out: dict | None = None) -> int:
+    """omprt_generic_reduce_host, with tgt_target's status: 0 ran (cell and
+    team_offsets updated), 2 device trap (out["trap"] = (TrapKind.value,
+    detail), host buffers untouched)."""
+    xp, n, dt = _host_ptr(x, "generic_reduce_host")
+    cp, _, dc = _host_ptr(cell, "generic_reduce_host")
+    if dc != dt:
+        raise TypeError("cell and x must have one element type")
+    op_ = None
+    if team_offsets is not None:
+        op_, no, do = _host_ptr(team_offsets, "generic_reduce_host")
+        if do != _lib.I64 or no < teams:
+            raise TypeError("team_offsets must be an int64 array of >= teams entries")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    _lib.ensure_device(dev.index)
+    st = _lib.check(_lib.load().omprt_generic_reduce_host(
+        C.c_void_p(xp), n, dt, _code(_lib.OP_NAMES, op), teams, par_threads, int(ordered),
+        pad_bytes, int(heap_fallback), heap_bytes_per_team, C.c_void_p(cp),
+        C.c_void_p(op_ or 0)), "omprt_generic_reduce_host")
+    if st == _lib.TRAP:
+        trap = runtime.check_trap(dev)
+        if trap is not None:
+            return _trap_status(trap, out)
+        return 2
+    return st

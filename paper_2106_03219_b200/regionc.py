@@ -533,7 +533,7 @@ def nvrtc_compile(src: str, name: str = "region.cu", lineinfo: bool = True) -> b
     prog = ctypes.c_void_p()
     _check(lib, lib.nvrtcCreateProgram(ctypes.byref(prog), src.encode(), name.encode(),
                                        0, None, None), "nvrtcCreateProgram")
-    opts = [f"--gpu-architecture={ARCH}", "-std=c++17", "-default-device",
+    opts = [f"--gpu-architecture={ARCH}", "-std=c++17", "-default-device", "--device-int128",
             "-diag-suppress=177,550"]
     if lineinfo:
         opts.append("-lineinfo")

@@ -76,6 +76,18 @@ def _dev(t: torch.Tensor) -> torch.device:
     return t.device
 
 
+def _check_range(lb: int, ub: int, *bufs: tuple[str, torch.Tensor]) -> None:
+    """Every buffer the loop body touches must hold iterations [lb, ub] — the
+    device kernels index x[i] without a size, so an escape here would read or
+    write past the allocation; the vgpu traps OutOfBounds on the same access
+    (vgpu.py:28-36).  An empty space (ub < lb) touches nothing."""
+    if ub < lb:
+        return
+    for name, t in bufs:
+        if lb < 0 or ub >= t.numel():
+            raise IndexError(f"iteration space [{lb}, {ub}] escapes {name}[0:{t.numel()}]")
+
+
 def _p(t: torch.Tensor | None) -> C.c_void_p:
     return C.c_void_p(0 if t is None else t.data_ptr())
 
@@ -89,7 +101,12 @@ def num_sms(index: int | None = None) -> int:
         torch.cuda.current_device() if torch.cuda.is_available() else -1)
     n = _sms.get(dev)
     if n is None:
-        n = _sms[dev] = check(_lib.load().omprt_num_sms(), "omprt_num_sms")
+        if dev == torch.cuda.current_device():
+            n = check(_lib.load().omprt_num_sms(), "omprt_num_sms")
+        else:
+            with torch.cuda.device(dev):
+                n = check(_lib.load().omprt_num_sms(), "omprt_num_sms")
+        _sms[dev] = n
     return n
 
 
@@ -221,12 +238,14 @@ class Trace:
 
     def __enter__(self):
         torch.cuda.synchronize(self.device)
-        check(_lib.load().omprt_set_trace(_p(self.buf), self.capacity), "omprt_set_trace")
+        with torch.cuda.device(self.device):  # the ring symbol is per device
+            check(_lib.load().omprt_set_trace(_p(self.buf), self.capacity), "omprt_set_trace")
         return self
 
     def __exit__(self, *exc):
         torch.cuda.synchronize(self.device)
-        check(_lib.load().omprt_set_trace(None, 0), "omprt_set_trace")
+        with torch.cuda.device(self.device):
+            check(_lib.load().omprt_set_trace(None, 0), "omprt_set_trace")
         raw = self.buf.cpu().numpy().view(np.uint8).view(TRACE_REC)
         self.records = raw[raw["kind"] != 0].copy()
         return False
@@ -299,8 +318,7 @@ def reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = None, sch
     m = _code(_lib.MODE_NAMES, mode)
     if ub is None:
         ub = lb + x.numel() - 1
-    if ub >= lb and (lb < 0 or ub >= x.numel()):
-        raise IndexError(f"iteration space [{lb}, {ub}] escapes x[0:{x.numel()}]")
+    _check_range(lb, ub, ("x", x))
     g = default_grid(dev)
     teams = teams or g.teams
     threads = threads or g.threads
@@ -325,8 +343,11 @@ def axpy_minmax(a: float, x: torch.Tensor, y: torch.Tensor, *, lb: int = 0, ub: 
     dev = _dev(x)
     if x.dtype != torch.float32 or y.dtype != torch.float32:
         raise TypeError("axpy_minmax is fp32")
+    if not (x.is_contiguous() and y.is_contiguous()) or y.device != dev:
+        raise ValueError("x and y must be contiguous and on one device")
     if ub is None:
         ub = lb + x.numel() - 1
+    _check_range(lb, ub, ("x", x), ("y", y))
     g = default_grid(dev)
     teams = teams or g.teams
     threads = threads or g.threads
@@ -351,8 +372,11 @@ def dot(x: torch.Tensor, y: torch.Tensor, *, lb: int = 0, ub: int | None = None,
     dev = _dev(x)
     if x.dtype != torch.float64 or y.dtype != torch.float64:
         raise TypeError("dot is fp64")
+    if not (x.is_contiguous() and y.is_contiguous()) or y.device != dev:
+        raise ValueError("x and y must be contiguous and on one device")
     if ub is None:
         ub = lb + x.numel() - 1
+    _check_range(lb, ub, ("x", x), ("y", y))
     g = default_grid(dev)
     teams = teams or g.teams
     threads = threads or g.threads
@@ -388,8 +412,13 @@ def generic_reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = N
     """Generic-mode region with __kmpc_alloc_shared globalisation and a nested
     parallel reduce (config 4).  Does not synchronise; call check_trap()."""
     dev = _dev(x)
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
     if ub is None:
         ub = lb + x.numel() - 1
+    _check_range(lb, ub, ("x", x))
+    if team_offsets is not None and team_offsets.numel() < teams:
+        raise IndexError(f"team_offsets holds {team_offsets.numel()} < {teams} teams")
     if out is None:
         out = torch.zeros(1, dtype=x.dtype, device=dev)
     L = _lib.load()

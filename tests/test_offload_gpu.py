@@ -146,3 +146,74 @@ def test_reduce_host_entry(cuda):
     c2 = np.zeros(1, np.float64)
     reduce_host(xn, c2, teams=148, threads=256, mode="ordered")
     assert c2[0] == O.reduce(xn, 0, n - 1, O.F64, O.ADD, O.STATIC, 1, 148, 256)
+
+
+def test_axpy_dot_generic_host_entries(cuda):
+    """The host-buffer C entries for configs 3, 5 and 4: copy-in, launch,
+    copy-out only on status 0 (host.py:276-295), bit-exact vs the oracle."""
+    from paper_2106_03219_b200 import axpy_minmax_host, dot_host, generic_reduce_host
+
+    n = (1 << 20) + 37
+    x = O.fill(n, O.F32, O.SEED, 2)
+    y = O.fill(n, O.F32, O.SEED, 3)
+    yo = y.copy()
+    mx, mn = O.axpy_minmax(2.5, x, yo, 0, n - 1, O.STATIC_CHUNKED, 64, 148, 384, -np.inf, np.inf)
+    cells = np.array([-np.inf, np.inf], np.float32)
+    yt = torch.from_numpy(y.copy()).pin_memory()
+    axpy_minmax_host(2.5, torch.from_numpy(x).pin_memory(), yt, cells, sched="static_chunked",
+                     chunk=64, teams=148, threads=384)
+    assert np.array_equal(yt.numpy(), yo)
+    assert cells[0] == mx and cells[1] == mn
+
+    xd, yd = O.fill(n, O.F64, O.SEED, 0), O.fill(n, O.F64, O.SEED, 1)
+    c = np.array([1.5], np.float64)
+    dot_host(xd, yd, c, teams=148, threads=384, mode="ordered")
+    assert c[0] == O.dot(xd, yd, 0, n - 1, O.STATIC, 1, 148, 384, 1.5)
+
+    xi = O.fill(n, O.I64, O.SEED, 4)
+    cell = np.array([9], np.int64)
+    offs = np.full(64, -1, np.int64)
+    assert generic_reduce_host(xi, cell, teams=64, par_threads=128, team_offsets=offs) == 0
+    assert cell[0] == O.generic_reduce(xi, 0, n - 1, O.I64, O.ADD, 64, 128, 9)
+    assert (offs == 0).all()  # parts is the team's first (and only) allocation
+    # an arena overflow traps: status 2, cell and offsets untouched
+    out = {}
+    cell2 = np.array([9], np.int64)
+    offs2 = np.full(64, -1, np.int64)
+    assert generic_reduce_host(xi, cell2, teams=64, par_threads=128, pad_bytes=65536 - 64,
+                               team_offsets=offs2, out=out) == 2
+    assert out["trap"][0] == "SharedOverflow"
+    assert cell2[0] == 9 and (offs2 == -1).all()
+
+
+def test_iteration_space_escape_is_out_of_bounds(cuda):
+    """A trip count larger than a buffer: the vgpu traps OutOfBounds (status 2,
+    buffers untouched); the B200 boundary refuses before any launch."""
+    from paper_2106_03219_b200 import runtime
+
+    x = torch.zeros(100, dtype=torch.float32, device=cuda)
+    y = torch.zeros(50, dtype=torch.float32, device=cuda)
+    with pytest.raises(IndexError):
+        runtime.axpy_minmax(1.0, x, y)  # ub = 99 escapes y[0:50]
+    with pytest.raises(IndexError):
+        runtime.dot(x.double(), y.double())
+    with pytest.raises(IndexError):
+        runtime.reduce(x, lb=-1, ub=10)
+    with pytest.raises(IndexError):
+        runtime.generic_reduce(x.double(), ub=100, teams=4, par_threads=32)
+    runtime.dot(x.double(), y.double(), ub=-1)  # an empty space touches nothing
+
+    args = (ArgDescriptor("n", "scalar", "i64"), ArgDescriptor("y", "buffer", "f32"),
+            ArgDescriptor("a", "scalar", "f32"), ArgDescriptor("x", "buffer", "f32"),
+            ArgDescriptor("mx", "buffer", "f32"), ArgDescriptor("mn", "buffer", "f32"))
+    call = TargetCall(1, kernel_name(1), args)
+    image = {"b200": {kernel_name(1): RegionKernel(
+        "axpy_minmax", {"a": "a", "x": "x", "y": "y", "max": "mx", "min": "mn", "n": "n"})}}
+    yb = le(range(50), np.float32)
+    mxb = le([-1.0], np.float32)
+    out = {}
+    st = tgt_target(call.bind([100, yb, 2.0, le(range(100), np.float32), mxb,
+                               le([1.0], np.float32)]), image, grid=(2, 32), out=out)
+    assert st == 2 and out["trap"][0] == "OutOfBounds"
+    assert np.array_equal(np.frombuffer(yb, np.float32), np.arange(50, dtype=np.float32))
+    assert np.frombuffer(mxb, np.float32)[0] == -1.0
