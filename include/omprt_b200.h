@@ -60,8 +60,15 @@ enum omprt_sched {
 
 /* ---- execution modes for the reductions.
  *  SPMD     every thread runs the loop; the lanes of a team cover the team's
- *           iterations with coalesced 16-byte vector loads (a legal
- *           re-association; integer results stay bit-exact)
+ *           iterations with coalesced 16-byte vector loads, and for the flat
+ *           chunked schedule the CTAs take balanced contiguous pieces of
+ *           [lb, ub] (a legal re-association: every iteration runs exactly
+ *           once; integer results stay bit-exact).  Floating-point sums are
+ *           within the stated tolerance (1e-6 fp64, 1e-4 fp32); fp max/min
+ *           return the exact extreme value, but when +0.0 and -0.0 tie for it
+ *           the sign of the returned zero is unspecified (step_max keeps the
+ *           first of tied values, and which zero comes first depends on the
+ *           order).  Use ORDERED for the reference order's zero sign.
  *  ORDERED  every device thread runs exactly its own schedule chunks in
  *           iteration order and the per-thread partials are combined in
  *           global thread order — the host fallback's order (host.py:567-582),

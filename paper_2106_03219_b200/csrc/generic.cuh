@@ -209,14 +209,50 @@ __global__ void k_arena_replay(const int64_t *__restrict__ script, int nops, int
 enum : int { kWorkExit = 0, kWorkRegion = 1 };
 
 constexpr uint32_t kBarFork = 1, kBarRegion = 2, kBarJoin = 3;
+constexpr int kGenericOrdDepth = 4;  // ORDERED workers: 32-byte loads in flight per lane
+
+// The team partials folded into acc strictly in team order (the fallback's
+// combine order, host.py:567-582) by one warp: the lanes load 128 partials
+// per round trip (coalesced, lane l holds b + 32k + l), then every lane walks
+// them in order through register shuffles — one dependent add per partial
+// instead of one L2 round trip per 8 (the single-thread fold_in_order was
+// ~45 us of C4's ORDERED launch at 1024 teams).  All 32 lanes call; the
+// result is the same in every lane.
+template <int OP, class T> OMPRT_D T warp_fold_in_order(T acc, const T *p, int64_t n) {
+  constexpr int K = 4;  // partials per lane per round trip (register budget of 32)
+  const uint32_t lane = lane_id();
+  for (int64_t b = 0; b < n; b += 32 * K) {
+    T v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t i = b + k * 32 + lane;
+      v[k] = i < n ? ld_cg(p + i) : Red<OP, T>::identity();
+    }
+    const int64_t m = n - b < 32 * K ? n - b : 32 * K;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int l = 0; l < 32; ++l) {
+        const T e = __shfl_sync(0xffffffffu, v[k], l);
+        if (k * 32 + l < m) acc = Red<OP, T>::apply(acc, e);
+      }
+    }
+  }
+  return acc;
+}
 
 // ORD: the ORDERED instance (its in-order worker loop needs more registers;
 // keeping it out of the SPMD instance keeps that one at 4 teams per SM).
 // TRACE: the instance with the trace-ring hooks, launched only while a ring
 // is installed (the hooks cost this kernel's short teams 4-6 % otherwise,
 // profiles/README.md).
-template <class T, int OP, int U, bool ORD = false, bool TRACE = false>
-__global__ void __launch_bounds__(kMaxThreads)
+// MAXT / MINB: the launch bound.  The default instance takes any P; the
+// one-wave instance (MAXT 288, MINB 7: at most 32 registers) is for teams of
+// 32 + P <= 288 threads, where seven teams fit per SM and C4's 1024 teams
+// (148 x 7 = 1036 slots) all run in a single wave instead of 1.7.
+template <class T, int OP, int U, bool ORD = false, bool TRACE = false, int MAXT = kMaxThreads,
+          int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB)
     k_generic(const T *__restrict__ x, int64_t lb, int64_t ub, int P, int ordered, int64_t pad,
               ArenaCfg cfg, Workspace ws, T *out, int64_t *team_offsets) {
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -288,8 +324,8 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (last) {
       fence_acq_rel_gpu();
       if constexpr (ORD) {
-        if (lane == 0 && !trap_raised())
-          *out = fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x);
+        const T v = warp_fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x);
+        if (lane == 0 && !trap_raised()) *out = v;
       } else {
         T v = Red<OP, T>::identity();
         for (uint32_t i = lane; i < gridDim.x; i += 32) v = Red<OP, T>::apply(v, ld_cg(partials + i));
@@ -310,7 +346,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         // for_static_init over the team block, literal sequential chunk
         int64_t mlb, mub;
         static_bounds(tlb, tub, wt, P, mlb, mub);
-        parts[wt] = fold_row_in_order<OP, T>(x, mlb, mub, Red<OP, T>::identity());
+        parts[wt] = fold_row_in_order<OP, T, kGenericOrdDepth>(x, mlb, mub, Red<OP, T>::identity());
       } else {
         // 256-bit streaming loads: the worker warps share the SM with other
         // teams, so each lane keeps U x 32 bytes in flight

@@ -247,8 +247,32 @@ struct AxpyBody {
 struct LoopArgs {
   int64_t lb, ub, chunk;
   int sched;
-  int split;  // SPMD: CTAs per OpenMP team (<= 1: one CTA per team)
+  int split;    // SPMD: CTAs per OpenMP team (<= 1: one CTA per team)
+  int balance;  // SPMD flat chunked: CTAs take balanced contiguous pieces
 };
+
+// Contiguous piece k of `cl` of [first, end): cut points on absolute
+// 64-element boundaries (16-byte aligned pieces for every element size).
+OMPRT_D void contiguous_piece(TeamSet &s, int64_t first, int64_t end, int64_t k, int64_t cl) {
+  const int64_t piece = (end - first + cl - 1) / cl;
+  auto cut = [&](int64_t j) {
+    if (j <= 0) return first;
+    if (j >= cl) return end;
+    int64_t c = (first + j * piece + 63) & ~(int64_t)63;
+    return c < end ? c : end;
+  };
+  const int64_t lo = cut(k), hi = cut(k + 1);
+  s.seg_stride = 0;
+  if (hi <= lo) {
+    s.nseg = 0;
+    s.seg_len = 0;
+    return;
+  }
+  s.first = lo;
+  s.seg_len = hi - lo;
+  s.nseg = 1;
+  s.ub = hi - 1;
+}
 
 // The iteration set of this CTA: its team's set (team_set, the schedule's
 // contract) — or, when a launch splits each team over `split` CTAs (few
@@ -260,31 +284,29 @@ struct LoopArgs {
 OMPRT_D TeamSet team_set_cta(const LoopArgs &la) {
   const int64_t cl = la.split > 1 ? la.split : 1;
   const int64_t teams = gridDim.x / cl, team = blockIdx.x / cl, sub = blockIdx.x % cl;
+  if (la.balance && la.sched == OMPRT_SCHED_STATIC_CHUNKED) {
+    // The flat chunked teeth of all teams tile [lb, ub] exactly once, so the
+    // union is contiguous: every CTA takes an equal contiguous piece of it
+    // (a per-team comb of ceil(N / (threads*chunk)) teeth over `teams` CTAs
+    // leaves a partial second wave, e.g. 171 teeth on 148 CTAs at C3's
+    // 148 x 384 x 4096).  Same iterations, each exactly once; integers are
+    // exact, max/min order-free, fp sums re-associated (SPMD).
+    TeamSet s;
+    s.ub = la.ub;
+    if (la.ub < la.lb) {
+      s.first = la.lb;
+      s.seg_len = s.seg_stride = s.nseg = 0;
+      return s;
+    }
+    contiguous_piece(s, la.lb, la.ub + 1, blockIdx.x, gridDim.x);
+    return s;
+  }
   TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, team, teams, blockDim.x);
   if (cl == 1 || s.nseg <= 0) return s;
   if (s.seg_stride == 0 || s.nseg <= 1) {
     int64_t len = s.ub - s.first + 1;
     if (len > s.seg_len) len = s.seg_len;
-    const int64_t end = s.first + len;
-    const int64_t piece = (len + cl - 1) / cl;
-    // cut points on absolute 64-element boundaries (16-byte aligned pieces)
-    auto cut = [&](int64_t k) {
-      if (k <= 0) return s.first;
-      if (k >= cl) return end;
-      int64_t c = (s.first + k * piece + 63) & ~(int64_t)63;
-      return c < end ? c : end;
-    };
-    const int64_t lo = cut(sub), hi = cut(sub + 1);
-    if (hi <= lo) {
-      s.nseg = 0;
-      s.seg_len = 0;
-      return s;
-    }
-    s.first = lo;
-    s.seg_len = hi - lo;
-    s.nseg = 1;
-    s.seg_stride = 0;
-    s.ub = hi - 1;
+    contiguous_piece(s, s.first, s.first + len, sub, cl);
     return s;
   }
   if (sub >= s.nseg) {
@@ -388,21 +410,25 @@ OMPRT_D T fold_in_order_team(T acc, const T *p, int64_t n, T *buf, int cap) {
 // 256-byte L2 promotion: every DRAM access brings 256 B of the thread's own
 // row, which its next seven loads then find in L2 — the rows of a warp are
 // far apart, so without the promotion DRAM would see 32-byte pieces.
-template <int OP, class T>
+// D: 32-byte loads in flight per step (2 for the literal ORDERED walk; the
+// generic-mode ORDERED workers take 4 — their teams share the SM, so each
+// lane needs more bytes in flight).
+template <int OP, class T, int D = 2>
 OMPRT_D T fold_row_in_order(const T *__restrict__ x, int64_t lo, int64_t hi, T part) {
   constexpr int V = 32 / (int)sizeof(T);
   int64_t i = lo;
   for (; i <= hi && (((uintptr_t)(x + i)) & 31u) != 0; ++i) part = Red<OP, T>::apply(part, x[i]);
-  for (; i + 2 * V - 1 <= hi; i += 2 * V) {
-    const U8x32 a = ld_v8<kLoadNcL2_256B>(x + i);
-    const U8x32 b = ld_v8<kLoadNcL2_256B>(x + i + V);
-    T va[V], vb[V];
-    memcpy(va, &a, 32);
-    memcpy(vb, &b, 32);
+  for (; i + D * V - 1 <= hi; i += D * V) {
+    U8x32 r[D];
 #pragma unroll
-    for (int k = 0; k < V; ++k) part = Red<OP, T>::apply(part, va[k]);
+    for (int d = 0; d < D; ++d) r[d] = ld_v8<kLoadNcL2_256B>(x + i + d * V);
 #pragma unroll
-    for (int k = 0; k < V; ++k) part = Red<OP, T>::apply(part, vb[k]);
+    for (int d = 0; d < D; ++d) {
+      T v[V];
+      memcpy(v, &r[d], 32);
+#pragma unroll
+      for (int k = 0; k < V; ++k) part = Red<OP, T>::apply(part, v[k]);
+    }
   }
   for (; i <= hi; ++i) part = Red<OP, T>::apply(part, x[i]);
   return part;

@@ -192,6 +192,14 @@ int spmd_split(int teams) {
   return cl < cap ? cl : cap;
 }
 
+// SPMD iteration-to-CTA mapping: the team split above, and for the flat
+// chunked schedule balanced contiguous CTA pieces (team_set_cta).  Variant
+// kNoSplit keeps the literal mapping (one CTA per team, its comb of teeth).
+void spmd_prepare(LoopArgs &la, int teams) {
+  la.split = spmd_split(teams);
+  la.balance = g_variant == kNoSplit ? 0 : 1;
+}
+
 // ORDERED row-group kernels (ordered.cuh).  Each CTA = nw streaming warps +
 // the folder warp; one CTA per SM (the tile ring takes most of the shared
 // memory), never more CTAs than the warp groups need.  Every launch gets a
@@ -347,7 +355,7 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
       k_reduce_ordered<T, OP><<<teams, threads, 0, st>>>(xp, la, w, op);
     }
   } else {
-    la.split = spmd_split(teams);
+    spmd_prepare(la, teams);
     const int grid = teams * la.split;
     if (bulk_ok) {
       // default SPMD path: TMA bulk-copy stage ring
@@ -423,7 +431,7 @@ int launch_exchange_t(const void *x, LoopArgs la, int teams, int threads, Worksp
   const size_t smem = BulkSmem<kBulkStages, kBulkStageBytes>::bytes;
   int rc = set_smem(kern, smem);
   if (rc) return rc;
-  la.split = spmd_split(teams);
+  spmd_prepare(la, teams);
   kern<<<teams * la.split, threads, smem, st>>>((const T *)x, la, w, (T *)out, xc);
   return check_launch("omprt_reduce_exchange");
 }
@@ -508,6 +516,11 @@ int check_atomic(int kind, int dtype, const uint64_t *desired) {
   return OMPRT_OK;
 }
 
+// Generic mode: teams of up to 288 threads take the one-wave instance
+// (seven teams per SM); variant kGenericNoOneWave keeps the default one (A/B).
+constexpr int kGenericOneWaveThreads = 288;
+constexpr int kGenericNoOneWave = 45;
+
 template <class T, int OP>
 int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, int ordered,
                      int64_t pad, ArenaCfg cfg, Workspace w, void *out, int64_t *offs,
@@ -515,6 +528,9 @@ int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, in
   // the ORDERED instance only where order matters (fp): integer folds give
   // the same bits in any order (see launch_reduce_t) and take the SPMD one
   auto kern = g_trace_on ? k_generic<T, OP, 4, false, true> : k_generic<T, OP, 4, false>;
+  if (32 + P <= kGenericOneWaveThreads && g_variant != kGenericNoOneWave)
+    kern = g_trace_on ? k_generic<T, OP, 2, false, true, kGenericOneWaveThreads, 7>
+                      : k_generic<T, OP, 2, false, false, kGenericOneWaveThreads, 7>;
   if constexpr (std::is_floating_point<T>::value) {
     if (ordered) kern = g_trace_on ? k_generic<T, OP, 4, true, true> : k_generic<T, OP, 4, true>;
   }
@@ -841,7 +857,7 @@ int launch_axpy_spmd(float a, const float *d_x, float *d_y, LoopArgs la, int tea
                      Workspace w, float *d_max, float *d_min, cudaStream_t st) {
   int rc;
   const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
-  la.split = spmd_split(teams);
+  spmd_prepare(la, teams);
   if (bulk_ok) {
     auto kern = threads <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
                                : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
@@ -952,13 +968,13 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
       k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
     }
   } else if (bulk_ok) {
-    la.split = spmd_split(teams);
+    spmd_prepare(la, teams);
     auto kern = k_dot_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
     if ((rc = set_smem(kern, smem))) return rc;
     kern<<<teams * la.split, threads, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
   } else {
-    la.split = spmd_split(teams);
+    spmd_prepare(la, teams);
     if (g_unroll >= 8)
       k_dot<8><<<teams * la.split, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
     else

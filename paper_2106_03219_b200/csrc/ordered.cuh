@@ -70,6 +70,12 @@ OMPRT_D void st_release_gpu(uint64_t *p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+OMPRT_D uint64_t ld_relaxed_gpu(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 OMPRT_D uint64_t ld_acquire_gpu(const uint64_t *p) {
   uint64_t v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -249,6 +255,22 @@ OMPRT_D void ord_issue(OrdRow<W, 16 / sizeof(T)> &row, const T *const (&src)[NS]
   if (live) row.advance();
 }
 
+template <class T> OMPRT_D T shfl_any(T v, int src_or_delta, bool down) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte partials");
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long u;
+    memcpy(&u, &v, 8);
+    u = down ? __shfl_down_sync(0xffffffffu, u, src_or_delta) : __shfl_sync(0xffffffffu, u, src_or_delta);
+    memcpy(&v, &u, 8);
+  } else {
+    unsigned u;
+    memcpy(&u, &v, 4);
+    u = down ? __shfl_down_sync(0xffffffffu, u, src_or_delta) : __shfl_sync(0xffffffffu, u, src_or_delta);
+    memcpy(&v, &u, 4);
+  }
+  return v;
+}
+
 // Stream this warp's work through the ring; fold(rows, s, e) consumes this
 // lane's row offsets s..e of the current tile in order, fold.publish(g)
 // stores OpenMP thread g's running partial (fold.resume(g) reloads it).
@@ -349,7 +371,22 @@ OMPRT_D void ord_groups(const LoopArgs &la, int64_t teams, int64_t threads,
     }
     cp_async_wait(0);
     __syncwarp();
-    if (g < P) fold.publish(g);
+    if constexpr (Fold::kAssoc) {
+      // max/min: the group's last unit folds its 32 running partials as the
+      // left-biased tree (bit-identical to the in-order chain, see
+      // ord_folder) and publishes one group result for the folder
+      if (seg == 0 || sidx == seg - 1) {
+        typename Fold::P v = g < P ? fold.value() : fold.identity();
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) v = fold.comb(v, shfl_any(v, d, true));
+        if (lane == 0) ((typename Fold::P *)(flags + ngroups))[grp] = v;
+        fold.reset();
+      } else if (g < P) {
+        fold.publish(g);
+      }
+    } else if (g < P) {
+      fold.publish(g);
+    }
     // the lanes' partials, then the flag (release, gpu scope)
     __threadfence();
     __syncwarp();
@@ -369,8 +406,14 @@ template <class T, int V> OMPRT_D void lds_vec(T (&v)[V], const T *p) {
 // One row's in-order fold of a window: offsets s..e of `row`.
 template <class T, int OP, int W> struct OrdReduceFold {
   static constexpr int V = 16 / (int)sizeof(T);
+  static constexpr bool kAssoc = OP != OMPRT_OP_ADD;  // max/min: group trees
+  using P = T;
   T part;
   T *tp;
+  OMPRT_D T value() const { return part; }
+  OMPRT_D static T identity() { return Red<OP, T>::identity(); }
+  OMPRT_D static T comb(T a, T b) { return Red<OP, T>::apply(a, b); }
+  OMPRT_D void reset() { part = identity(); }
   OMPRT_D void operator()(const T *const (&rows)[1], int s, int e) {
     const T *r = rows[0];
     if (s == 0 && e == W - 1) {
@@ -393,6 +436,12 @@ template <class T, int OP, int W> struct OrdReduceFold {
 };
 
 template <int W> struct OrdDotFold {
+  static constexpr bool kAssoc = false;
+  using P = double;
+  OMPRT_D static double identity() { return 0.0; }
+  OMPRT_D static double comb(double a, double b) { return a + b; }
+  OMPRT_D double value() const { return part; }
+  OMPRT_D void reset() { part = 0.0; }
   double part;
   double *tp;
   OMPRT_D void operator()(const double *const (&rows)[2], int s, int e) {
@@ -451,22 +500,6 @@ OMPRT_D void ord_folder_load(const T *tp, int64_t P, const uint64_t *flags, uint
   for (int k = 0; k < N; ++k) L.v[k] = (first + k < P) ? ld_cg(tp + first + k) : T();
 }
 
-template <class T> OMPRT_D T shfl_any(T v, int src_or_delta, bool down) {
-  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "4- or 8-byte partials");
-  if constexpr (sizeof(T) == 8) {
-    unsigned long long u;
-    memcpy(&u, &v, 8);
-    u = down ? __shfl_down_sync(0xffffffffu, u, src_or_delta) : __shfl_sync(0xffffffffu, u, src_or_delta);
-    memcpy(&v, &u, 8);
-  } else {
-    unsigned u;
-    memcpy(&u, &v, 4);
-    u = down ? __shfl_down_sync(0xffffffffu, u, src_or_delta) : __shfl_sync(0xffffffffu, u, src_or_delta);
-    memcpy(&v, &u, 4);
-  }
-  return v;
-}
-
 // The folder warp: folds the P per-thread partials in global thread order
 // into acc.  For max/min (Combine::kAssoc) the reference's step
 // `acc < e ? e : acc` keeps the leftmost maximum of its operands (a partial
@@ -482,52 +515,37 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
   constexpr int N = FoldLoad<T>::N;
   const uint32_t lane = threadIdx.x & 31u;
   if constexpr (std::decay_t<Combine>::kAssoc) {
-    // Trees read only each lane's own 8 partials, so the batches stay in
-    // registers.  Four batches (32 groups) per step: lane l acquires group
-    // l's ready flag, the warp barrier orders every lane's partial loads
-    // after all 32 acquires, then the 4 x 8 loads per lane go out together
-    // — one flag round trip and one load round trip per 1024 partials.
-    static_assert(kFoldPer == 8 * 32, "eight groups of 32 partials per batch");
-    const int64_t nfull = P / kFoldPer;
-    FoldLoad<T> R0, R1, R2, R3;
-    auto ldb = [&](int64_t b, FoldLoad<T> &L) {
-      const T *q = tp + b * kFoldPer + (int64_t)lane * N;
+    // The streaming warps already folded every group's 32 partials as a
+    // left-biased tree (ord_groups); the folder takes the ngroups group
+    // results in order, kFoldB per lane per step: relaxed loads of the lane's
+    // ready flags (retried until all show this launch's epoch), one acquire
+    // fence, the lane's results folded in order, then the same tree across
+    // the lanes.  One flag and one data round trip per 256 groups.
+    const int64_t ng = (P + 31) / 32;
+    const T *gres = (const T *)(flags + ng);
+    for (int64_t b = 0; b < ng; b += 32 * kFoldB) {
+      const int64_t j0 = b + (int64_t)lane * kFoldB;
+      bool ready;
+      do {
+        ready = true;
 #pragma unroll
-      for (int k = 0; k < N; ++k) L.v[k] = ld_cg(q + k);
-    };
-    auto tree = [&](const FoldLoad<T> &L) {
-      T v = L.v[0];
+        for (int k = 0; k < kFoldB; ++k)
+          if (j0 + k < ng) ready &= ld_relaxed_gpu(flags + j0 + k) == epoch;
+      } while (!ready);
+      fence_acq_rel_gpu();
+      T r[kFoldB];
 #pragma unroll
-      for (int k = 1; k < N; ++k) v = comb(v, L.v[k]);
+      for (int k = 0; k < kFoldB; ++k) r[k] = j0 + k < ng ? ld_cg(gres + j0 + k) : comb.identity();
+      T v = r[0];
+#pragma unroll
+      for (int k = 1; k < kFoldB; ++k) v = comb(v, r[k]);
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) v = comb(v, shfl_any<T>(v, d, true));
       acc = comb(acc, shfl_any<T>(v, 0, false));
-    };
-    for (int64_t b = 0; b < nfull; b += 4) {
-      const int64_t nbat = nfull - b < 4 ? nfull - b : 4;
-      if ((int64_t)lane < nbat * 8)
-        while (ld_acquire_gpu(flags + b * 8 + lane) != epoch) {
-        }
-      __syncwarp();
-      ldb(b, R0);
-      if (nbat > 1) ldb(b + 1, R1);
-      if (nbat > 2) ldb(b + 2, R2);
-      if (nbat > 3) ldb(b + 3, R3);
-      tree(R0);
-      if (nbat > 1) tree(R1);
-      if (nbat > 2) tree(R2);
-      if (nbat > 3) tree(R3);
-    }
-    // the last, partial batch one by one (every lane folds the same values)
-    for (int64_t j = nfull * kFoldPer; j < P; ++j) {
-      if (j % 32 == 0 || j == nfull * kFoldPer)
-        while (ld_acquire_gpu(flags + j / 32) != epoch) {
-        }
-      acc = comb(acc, ld_cg(tp + j));
     }
     if (lane == 0)
       trace_record(gridDim.x * ((blockDim.x >> 5) - 1), kTraceFolder,
-                   (uint32_t)((P + kFoldPer - 1) / kFoldPer), trace_t0());
+                   (uint32_t)((ng + 32 * kFoldB - 1) / (32 * kFoldB)), trace_t0());
     return acc;
   }
   const int64_t nb = (P + kFoldPer - 1) / kFoldPer;
@@ -562,6 +580,7 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
 template <int OP, class T> struct RedComb {
   static constexpr bool kAssoc = OP != OMPRT_OP_ADD;  // leftmost max / min (ord_folder)
   OMPRT_D T operator()(T a, T b) const { return Red<OP, T>::apply(a, b); }
+  OMPRT_D static T identity() { return Red<OP, T>::identity(); }
 };
 
 // flags (one u64 per group) live after the P partials in the (2-slot)
@@ -627,8 +646,22 @@ __global__ void __launch_bounds__((kOrdMaxWarps + 1) * 32)
 // chains (independent, so interleaved at the latency of one).
 template <int W> struct OrdMinMaxFold {
   static constexpr int V = 4;
+  static constexpr bool kAssoc = true;
+  using P = float2;
   float mx, mn;
   float2 *tp;
+  OMPRT_D float2 value() const { return make_float2(mx, mn); }
+  OMPRT_D static float2 identity() {
+    return make_float2(Limits<float>::lowest(), Limits<float>::highest());
+  }
+  OMPRT_D static float2 comb(float2 a, float2 b) {
+    return make_float2(Red<OMPRT_OP_MAX, float>::apply(a.x, b.x),
+                       Red<OMPRT_OP_MIN, float>::apply(a.y, b.y));
+  }
+  OMPRT_D void reset() {
+    mx = Limits<float>::lowest();
+    mn = Limits<float>::highest();
+  }
   OMPRT_D void operator()(const float *const (&rows)[1], int s, int e) {
     const float *r = rows[0];
     if (s == 0 && e == W - 1) {
@@ -663,10 +696,8 @@ template <int W> struct OrdMinMaxFold {
 
 struct MinMaxComb {
   static constexpr bool kAssoc = true;
-  OMPRT_D float2 operator()(float2 a, float2 b) const {
-    return make_float2(Red<OMPRT_OP_MAX, float>::apply(a.x, b.x),
-                       Red<OMPRT_OP_MIN, float>::apply(a.y, b.y));
-  }
+  OMPRT_D float2 operator()(float2 a, float2 b) const { return OrdMinMaxFold<4>::comb(a, b); }
+  OMPRT_D static float2 identity() { return OrdMinMaxFold<4>::identity(); }
 };
 
 template <int W>

@@ -69,6 +69,52 @@ def test_axpy_config3_full_size(cuda):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("teams,threads", [(148, 384), (148, 1024)])
+def test_axpy_config3_flat_static_chunked_full_size(cuda, teams, threads):
+    # config 3 as the bench runs it: flat schedule(static, c) at N = 2^28,
+    # chunk 1/64/4096, in the bench geometry (148 x 384) and 148 x 1024;
+    # y bit for bit, max/min exact against the oracle's chunk walk
+    n = 1 << 28
+    xd = runtime.synthetic(n, "f32", O.SEED, 0, device=cuda)
+    x = xd.cpu().numpy()
+    y0 = O.fill(n, O.F32, O.SEED, 1)
+    for chunk in (1, 64, 4096):
+        for mode in ("spmd", "ordered"):
+            yd = torch.from_numpy(y0).to(cuda)
+            yo = y0.copy()
+            mx, mn = O.axpy_minmax(2.5, x, yo, 0, n - 1, O.STATIC_CHUNKED, chunk, teams, threads,
+                                   -np.inf, np.inf)
+            gmx, gmn = runtime.axpy_minmax(2.5, xd, yd, sched="static_chunked", chunk=chunk,
+                                           teams=teams, threads=threads, mode=mode)
+            assert float(gmx.item()) == mx and float(gmn.item()) == mn, (chunk, mode)
+            assert torch.equal(yd, torch.from_numpy(yo).to(cuda)), (chunk, mode)
+            del yd
+    torch.cuda.empty_cache()
+
+
+def test_axpy_spmd_signed_zero_rule(cuda):
+    # SPMD max/min return the exact extreme; when +0 and -0 tie for it the
+    # zero's sign is unspecified (include/omprt_b200.h, omprt_mode), so only
+    # the value is checked here; y stays bit-exact (ORDERED pins the sign:
+    # test_axpy_ordered_keeps_the_reference_order_of_signed_zeros)
+    n = 1 << 20
+    for base in (-1.0, 1.0):
+        x = np.zeros(n, dtype=np.float32)
+        y = np.full(n, base, dtype=np.float32)
+        i = np.arange(n)
+        x[(i % 997) == 5], y[(i % 997) == 5] = np.float32(-0.0), np.float32(-0.0)
+        x[(i % 1009) == 3], y[(i % 1009) == 3] = np.float32(0.0), np.float32(0.0)
+        yo = y.copy()
+        mx, mn = O.axpy_minmax(1.0, x, yo, 0, n - 1, O.STATIC_CHUNKED, 64, 148, 384,
+                               -np.inf, np.inf)
+        xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+        gmx, gmn = runtime.axpy_minmax(1.0, xd, yd, sched="static_chunked", chunk=64, teams=148,
+                                       threads=384)
+        assert float(gmx.item()) == mx and float(gmn.item()) == mn  # -0 == +0
+        assert (float(gmx.item()) == 0.0) == (base < 0) and (float(gmn.item()) == 0.0) == (base > 0)
+        assert np.array_equal(yd.cpu().numpy().view(np.uint32), yo.view(np.uint32))
+
+
 @pytest.mark.parametrize("sched", list(SCHEDS))
 def test_dot_matches_oracle(cuda, sched):
     n = 500_003

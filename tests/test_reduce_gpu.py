@@ -231,15 +231,22 @@ def test_comb_bulk_plans(cuda, dtype):
                                           (148, 256, 1, 0, n - 1), (2, 64, 4096, 0, 70_000),
                                           (4, 128, 2, 1, n - 1)):
         want = O.reduce(x, lb, ub, dt, O.ADD, O.STATIC_CHUNKED, chunk, teams, threads, 0)
-        out = torch.zeros(1, dtype=xd.dtype, device=cuda)
-        runtime.reduce(xd, lb=lb, ub=ub, sched="static_chunked", chunk=chunk, teams=teams,
-                       threads=threads, out=out)
-        got = out.cpu().numpy()[0]
-        if dt == O.F64:
-            exact = O.accurate_sum_f64(x[lb:ub + 1])
-            assert abs(float(got) - exact) <= 1e-9 * exact
-        else:
-            assert int(got) == int(want), (teams, threads, chunk, lb, ub)
+        # default: balanced contiguous CTA pieces; variant 30: each team's
+        # literal comb of teeth through the comb bulk plans
+        for variant in (0, 30):
+            out = torch.zeros(1, dtype=xd.dtype, device=cuda)
+            runtime.set_variant(variant)
+            try:
+                runtime.reduce(xd, lb=lb, ub=ub, sched="static_chunked", chunk=chunk,
+                               teams=teams, threads=threads, out=out)
+            finally:
+                runtime.set_variant(0)
+            got = out.cpu().numpy()[0]
+            if dt == O.F64:
+                exact = O.accurate_sum_f64(x[lb:ub + 1])
+                assert abs(float(got) - exact) <= 1e-9 * exact
+            else:
+                assert int(got) == int(want), (teams, threads, chunk, lb, ub, variant)
 
 
 @pytest.mark.parametrize("sched", list(SCHEDS))

@@ -81,7 +81,10 @@ def main():
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--cpu", action="store_true",
                     help="time the CPU reference (oracle port, all host cores) beside each config")
+    ap.add_argument("--sections", default="c1,c2,c5,c3,c4",
+                    help="comma-separated subset of c1,c2,c5,c3,c4")
     a = ap.parse_args()
+    want = set(a.sections.split(","))
     if a.cpu:
         from oracle import oracle as O
 
@@ -91,6 +94,19 @@ def main():
     dev = torch.device("cuda", 0)
     sms = runtime.num_sms()
 
+    if "c1" in want:
+        c1_lines(a, dev, sms)
+    if "c2" in want or "c5" in want:
+        c2_c5_lines(a, dev, sms, want)
+    if "c3" in want:
+        c3_lines(a, dev, sms)
+    if "c4" in want:
+        c4_lines(a, dev, sms)
+
+
+def c1_lines(a, dev, sms):
+    if CPU["on"]:
+        from oracle import oracle as O
     # C1: static partition + int64 sum, 1 team x 128 threads, N = 2^20
     n = 1 << 20
     x = runtime.synthetic(n, "i64", SEED, device=dev)
@@ -107,6 +123,10 @@ def main():
          note="L2-resident after the first pass")
     del x
 
+
+def c2_c5_lines(a, dev, sms, want):
+    if CPU["on"]:
+        from oracle import oracle as O
     # C2: fp64 sum 2^30 (the headline; ordered mode for reference)
     n = 1 << 30
     x = runtime.synthetic(n, "f64", SEED, device=dev)
@@ -149,6 +169,10 @@ def main():
     del x, y, xi
     torch.cuda.empty_cache()
 
+
+def c3_lines(a, dev, sms):
+    if CPU["on"]:
+        from oracle import oracle as O
     # C3: chunked static axpy + fp32 max/min, N=2^28 (read x, read y, write y)
     n = 1 << 28
     xs = runtime.synthetic(n, "f32", SEED, 0, device=dev)
@@ -169,9 +193,30 @@ def main():
                                                    runtime.DEFAULT_THREADS,
                                                    float("-inf"), float("inf")), ns * 12)
             line(f"C3 axpy+max/min {sched} chunk={chunk} N=2^28", ms, n * 12, cpu=c3)
+    # the same at 148 x 1024, and ORDERED mode (reference order of max/min)
+    for chunk in (1, 64, 4096):
+        ms = timeit(lambda: runtime.axpy_minmax(1e-7, xs, ys, sched="static_chunked", chunk=chunk,
+                                                teams=sms, threads=1024, out_max=mx, out_min=mn),
+                    a.reps // 2)
+        line(f"C3 axpy+max/min static_chunked chunk={chunk} N=2^28", ms, n * 12, teams=sms,
+             threads=1024)
+    for thr in (384, 1024):
+        for chunk in (64, 4096):
+            ms = timeit(lambda: runtime.axpy_minmax(1e-7, xs, ys, sched="static_chunked",
+                                                    chunk=chunk, teams=sms, threads=thr,
+                                                    mode="ordered", out_max=mx, out_min=mn),
+                        a.reps // 4, 5)
+            line(f"C3 axpy+max/min static_chunked chunk={chunk} ORDERED N=2^28", ms, n * 12,
+                 teams=sms, threads=thr,
+                 note="two passes: axpy (12 B/elem) + the ORDERED max/min pass over y (4 B/elem); "
+                      "GB/s counts the algorithmic 12 B/elem")
     del xs, ys
     torch.cuda.empty_cache()
 
+
+def c4_lines(a, dev, sms):
+    if CPU["on"]:
+        from oracle import oracle as O
     # C4: generic mode, __kmpc_alloc_shared globalisation, 1024 teams, x[2^26]
     n = 1 << 26
     for dtype in ("i64", "f64"):

@@ -66,7 +66,7 @@ def _num(v: str) -> float | None:
         return None
 
 
-def report(path: str, out: str, algorithmic: float | None) -> dict:
+def report(path: str, out: str, algorithmic: float | None, meta: dict | None = None) -> dict:
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -93,7 +93,7 @@ def report(path: str, out: str, algorithmic: float | None) -> dict:
                 rec["algorithmic_bytes_per_launch"] = algorithmic
                 rec["traffic_over_algorithmic"] = (rd + wr) / algorithmic
         launches.append(rec)
-    res = {"source": path, "launches": launches}
+    res = {"source": path, **(meta or {}), "launches": launches}
     if launches:
         res["dram_bytes_per_launch"] = launches[0].get("dram_bytes_per_launch")
     with open(out, "w") as f:
@@ -126,5 +126,10 @@ if __name__ == "__main__":
     alg = None
     if "--algorithmic-bytes" in sys.argv:
         alg = float(sys.argv[sys.argv.index("--algorithmic-bytes") + 1])
-    r = report(src, dst, alg) if mode == "report" else launches(src, dst)
+    meta = {}
+    # --meta <json>: provenance written next to the capture on the GPU box
+    # (captured_at UTC, lib_sha16 of the libomprt_b200.so that ran)
+    if "--meta" in sys.argv:
+        meta = json.load(open(sys.argv[sys.argv.index("--meta") + 1]))
+    r = report(src, dst, alg, meta) if mode == "report" else launches(src, dst)
     print(json.dumps(r, indent=1)[:3000])
