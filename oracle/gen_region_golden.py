@@ -427,10 +427,17 @@ def main() -> None:
         r = runs[0]
         for o in runs[1:]:
             assert (o.stdout, o.stderr, o.exit_status) == (r.stdout, r.stderr, r.exit_status), name
-        out["programs"].append({"name": name, "source": src, "kwargs": kw,
-                                "stdout": r.stdout, "stderr": r.stderr,
-                                "exit_status": r.exit_status,
-                                "offloads": [list(x) for x in r.offloads]})
+        rec = {"name": name, "source": src, "kwargs": kw,
+               "stdout": r.stdout, "stderr": r.stderr,
+               "exit_status": r.exit_status,
+               "offloads": [list(x) for x in r.offloads]}
+        if r.exit_status == 0:
+            # executed IR instructions per region (host.py:524-528): the sum
+            # over threads, the same under every seed when nothing traps
+            for o in runs[1:]:
+                assert o.device_instructions == r.device_instructions, name
+            rec["device_instructions"] = [list(x) for x in r.device_instructions]
+        out["programs"].append(rec)
         print(f"{name:28s} exit={r.exit_status} {r.stderr.strip()[:90]}")
     dst = ROOT / "tests" / "golden" / "region_programs.json"
     dst.write_text(json.dumps(out, indent=1) + "\n")

@@ -72,7 +72,13 @@ struct RtCtx {
   u8 *gshadow;      // their init shadow (check_uninit) or null
   u8 *sshadow;      // this team's team-shared init shadow or null
   u32 *waitmask;    // per team 32 words: threads caught in a dead barrier
+  u64 seed;         // sched_seed (0: the hardware's own interleaving)
 };
+
+// The launch record after the trap (regions.launch allocates 128 bytes):
+// byte 56 the executed-IR-instruction counter (vgpu ExecResult
+// .instruction_count, vgpu.py:390), byte 64 the sched_seed.
+constexpr u32 kRtCountOff = 56, kRtSeedOff = 64;
 
 __shared__ RtCtx rt_ctx;
 
@@ -125,6 +131,29 @@ __device__ __noinline__ void rt_barrier(u32 site) {
 
 // the end of the region for this thread: a finished thread
 RT_D void rt_finish() { (void)rt_bar_or(1u); }
+
+// This thread's executed IR instructions (every basic block adds its length
+// on entry, as the vgpu counts one per _step) into the launch's counter.
+RT_D void rt_count(u64 n) {
+  atomicAdd((unsigned long long *)((u8 *)rt_ctx.trap + kRtCountOff), (unsigned long long)n);
+}
+
+// Seeded interleaving (the vgpu's sched_seed, vgpu.py:285-306): with a
+// nonzero seed every thread sleeps a splitmix64-drawn 0..2047 ns before each
+// atomic and barrier, keyed by (seed, team, thread, instructions executed so
+// far), so a seed perturbs which thread reaches a racing operation first and
+// different seeds explore different orders.  The hardware still decides the
+// final order, so a seed does not replay a schedule bit for bit; seed 0 keeps
+// the hardware's own interleaving.
+RT_D void rt_jitter(u64 k) {
+  const u64 seed = rt_ctx.seed;
+  if (seed == 0) return;
+  u64 z = seed ^ ((u64)blockIdx.x << 40) ^ ((u64)threadIdx.x << 20) ^ (k * 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  __nanosleep((u32)(z & 2047u));
+}
 
 RT_D u64 rt_label(const P &p) { return ((u64)p.space << 32) | p.label; }
 
@@ -387,6 +416,7 @@ RT_D void rt_prologue(const u64 *v, u32 shared_bytes) {
     rt_ctx.gshadow = (u8 *)v[2];
     rt_ctx.sshadow = v[3] ? (u8 *)v[3] + (u64)blockIdx.x * shared_bytes : nullptr;
     rt_ctx.waitmask = (u32 *)v[4];
+    rt_ctx.seed = *(const u64 *)((const u8 *)v[0] + kRtSeedOff);
   }
   for (u32 i = threadIdx.x; i < shared_bytes; i += blockDim.x) rt_team_shared[i] = 0xAA;
   __syncthreads();

@@ -298,7 +298,7 @@ def b200_tgt_target(call, bundle, device="vgpu", force_fail: bool = False, *, gr
     image = image_for(bundle, call)
     if image is None or call.kernel_id not in image.kernels:
         return 1
-    return _run_image(image, call, teams, threads, check_uninit, out)
+    return _run_image(image, call, teams, threads, check_uninit, out, sched_seed)
 
 
 def _run_recognised(call, teams: int, threads: int, out: dict | None,
@@ -370,8 +370,10 @@ def _run_recognised(call, teams: int, threads: int, out: dict | None,
 
 
 def _run_image(image, call, teams: int, threads: int, check_uninit: bool,
-               out: dict | None) -> int:
-    """tgt_target's marshalling (host.py:276-295) around regions.launch."""
+               out: dict | None, sched_seed: int = 0) -> int:
+    """tgt_target's marshalling (host.py:276-295) around regions.launch.
+    out["result"] carries the launch's instruction_count, which forge's host
+    program records in device_instructions (host.py:524-528)."""
     from forge import host as H
 
     packed: list[object] = []
@@ -381,10 +383,10 @@ def _run_image(image, call, teams: int, threads: int, check_uninit: bool,
         else:
             packed.append(bytearray(H._pack_arg(desc, v)))
     res = regions.launch(image, call.kernel_id, (teams, threads), packed,
-                         check_uninit=check_uninit)
+                         check_uninit=check_uninit, sched_seed=sched_seed)
     if out is not None:
         out["trace"] = []
-        out["result"] = None
+        out["result"] = res
     if res.status == "trap":
         if out is not None:
             out["trap"] = (res.trap, res.trap_detail)

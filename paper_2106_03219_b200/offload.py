@@ -207,8 +207,11 @@ def tgt_target(call: TargetCall, bundle, device="b200", force_fail: bool = False
 
     bundle: {"b200": {kernel_id: RegionKernel}}.  On 0 the buffer arguments
     hold the device results; on nonzero status they are untouched.
-    sched_seed / check_uninit are accepted for signature compatibility
-    (hardware scheduling has no seed).  collect_trace=True
+    sched_seed / check_uninit are accepted for signature compatibility: a
+    construct kernel's result does not depend on the interleaving (its
+    combine is the ticketed team-order fold).  Compiled regions
+    (forge_bridge, regions.launch) honour both: sched_seed jitters every
+    thread before its atomics and barriers (rt_jitter).  collect_trace=True
     records the construct's per-team device trace (runtime.Trace) into
     out["trace"] — team start/SM, the ticket each team's atom.inc took, the
     ordered combine — in the vgpu's "seq team thread kind detail" format.

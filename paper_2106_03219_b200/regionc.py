@@ -279,7 +279,7 @@ class _Translator:
                 raise RegionCompileError(f"@{f.name}: value {tok} used before definition")
             return names[key]
 
-        params = []
+        params = ["u64 *__ic"]  # the thread's executed-instruction count
         for k, (pn, pt) in enumerate(f.params):
             names[pn] = f"a{k}"
             types[pn] = "P" if pt.startswith("ptr<") else "u64"
@@ -316,7 +316,7 @@ class _Translator:
                 tdecl.append(f"  {t} t{len(tdecl)};")
         body = []
         for bi, b in enumerate(f.blocks):
-            body.append(f"{b.label}:;")
+            body.append(f"{b.label}:; *__ic += {len(b.instrs)}ull;")
             for ins in b.instrs:
                 body.append("  " + self.instr(f, ins, vname, slots, order, bi))
         ret = self._ctype(f.ret)
@@ -389,7 +389,7 @@ class _Translator:
             callee = self.funcs.get(a[0][1:])
             if callee is None:
                 raise RegionCompileError(f"call to unknown function {a[0]}")
-            call = f"{self.fnames[callee.name]}({', '.join(v(x) for x in a[1:])})"
+            call = f"{self.fnames[callee.name]}({', '.join(['__ic'] + [v(x) for x in a[1:]])})"
             return f"{d} = {call};" if d is not None else f"{call};"
         if op == "ret":
             return f"return {v(a[0])};" if a else "return;"
@@ -408,18 +408,19 @@ class _Translator:
             ss = self.site(kind="access", what="atomic store")
             dd = v(a[2]) if kind == "cas" else "0ull"
             sgn = "true" if ty in _SIGNED else "false"
-            return put(f"rt_atomic({v(a[0])}, {_ATOMICS[kind]}u, {sgn}, {_SIZES[ty]}u, "
+            return "rt_jitter(*__ic); " + put(f"rt_atomic({v(a[0])}, {_ATOMICS[kind]}u, {sgn}, {_SIZES[ty]}u, "
                        f"{v(a[1])}, {dd}, {sl}, {ss})")
         if op in _INC:
             sl = self.site(kind="access", what="atomic load")
             ss = self.site(kind="access", what="atomic store")
-            return put(f"rt_atomic({v(a[0])}, 5u, false, 4u, {v(a[1])}, 0ull, {sl}, {ss})")
+            return "rt_jitter(*__ic); " + put(
+                f"rt_atomic({v(a[0])}, 5u, false, 4u, {v(a[1])}, 0ull, {sl}, {ss})")
         if op in _FENCE:
             return "__threadfence();"
         if op in _BARRIER:
             self.has_barrier = True
             s = self.site(kind="deadlock")
-            return f"rt_barrier({s});"
+            return f"rt_jitter(*__ic); rt_barrier({s});"
         if op in _TRAP:
             s = self.site(kind="trap", func=f.name)
             c = v(a[0])
@@ -459,7 +460,8 @@ class _Translator:
              f'extern "C" __global__ void __launch_bounds__(1024) {k.name}(const A_{k.name} a) {{',
              f"  rt_prologue(a.v, {self.ssize}u);"] + inits +
             ["  __syncthreads();"] + unpack +
-            [f"  {self.fnames[k.name]}({', '.join(args)});", "  rt_finish();", "}"])
+            ["  u64 ic = 0;", f"  {self.fnames[k.name]}({', '.join(['&ic'] + args)});",
+             "  rt_count(ic);", "  rt_finish();", "}"])
         return src, {"params": [list(p) for p in k.params], "argv_slots": slots}
 
     def translate(self) -> tuple[str, dict]:

@@ -43,7 +43,7 @@ class RegionResult:
     trap_detail: str = ""
     buffers: list = field(default_factory=list)   # bytes per buffer arg (None: scalar)
     globals: dict = field(default_factory=dict)   # global-space globals after the launch
-    instruction_count: int = 0       # not counted on hardware
+    instruction_count: int = 0       # IR instructions executed by all threads (vgpu.py:390)
 
 
 _handles: dict[tuple[str, int], int] = {}
@@ -123,9 +123,14 @@ def _global_blob(image: B200Image, check_uninit: bool) -> tuple[bytearray, bytea
 
 
 def launch(image: B200Image, kernel: str, grid: tuple[int, int], args: list,
-           *, check_uninit: bool = False, device: torch.device | None = None) -> RegionResult:
+           *, check_uninit: bool = False, device: torch.device | None = None,
+           sched_seed: int = 0) -> RegionResult:
     """Run `kernel` of `image` on (teams x threads) with vgpu-packed args
-    (bytes/bytearray per buffer, int per scalar; vgpu.launch's contract)."""
+    (bytes/bytearray per buffer, int per scalar; vgpu.launch's contract).
+    `instruction_count` is the IR instructions every thread executed (exact
+    for launches that complete; the vgpu's count, vgpu.py:390); a nonzero
+    `sched_seed` perturbs the interleaving at atomics and barriers
+    (rt_jitter, csrc/region_rt.cuh)."""
     info = image.kernels.get(kernel)
     if info is None:
         raise ValueError(f"no function '{kernel}' in the image")
@@ -153,7 +158,10 @@ def launch(image: B200Image, kernel: str, grid: tuple[int, int], args: list,
     d_gsh = torch.frombuffer(gshadow, dtype=torch.uint8).to(dev) if gshadow is not None else None
     d_ssh = (torch.zeros(max(teams * shared, 1), dtype=torch.uint8, device=dev)
              if check_uninit and shared else None)
-    d_trap = torch.zeros(64, dtype=torch.uint8, device=dev)
+    # launch record: the trap (56 B), the instruction counter, the seed
+    rec0 = bytearray(128)
+    struct.pack_into("<Q", rec0, 64, int(sched_seed) & ((1 << 64) - 1))
+    d_trap = torch.frombuffer(rec0, dtype=torch.uint8).to(dev)
     d_wait = torch.zeros(teams * 32, dtype=torch.int32, device=dev)
 
     words = [d_trap.data_ptr(), d_blob.data_ptr(), d_gsh.data_ptr() if d_gsh is not None else 0,
@@ -187,9 +195,11 @@ def launch(image: B200Image, kernel: str, grid: tuple[int, int], args: list,
                                     8 * len(words), C.c_void_p(stream.cuda_stream)),
                "omprt_image_launch")
     rec = bytes(d_trap.cpu().numpy())  # synchronises the stream
+    count = struct.unpack_from("<Q", rec, 56)[0]
     if struct.unpack_from("<I", rec, 0)[0]:
-        name, detail = render_trap(image, rec, d_wait.cpu(), teams, threads)
-        return RegionResult("trap", name, detail, [None] * len(args))
+        # (the count of a trapped launch covers the threads that finished)
+        name, detail = render_trap(image, rec[:56], d_wait.cpu(), teams, threads)
+        return RegionResult("trap", name, detail, [None] * len(args), instruction_count=count)
     out = [bytes(t.cpu().numpy()) if t is not None else None for t in bufs]
     gvals = {}
     host_blob = bytes(d_blob.cpu().numpy())
@@ -200,4 +210,4 @@ def launch(image: B200Image, kernel: str, grid: tuple[int, int], args: list,
         vals = [int.from_bytes(host_blob[g["off"] + i * w:g["off"] + (i + 1) * w], "little")
                 for i in range(g["count"])]
         gvals[g["name"]] = vals[0] if g["count"] == 1 else vals
-    return RegionResult("ok", None, "", out, gvals)
+    return RegionResult("ok", None, "", out, gvals, instruction_count=count)

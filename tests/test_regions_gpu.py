@@ -250,3 +250,71 @@ void kernel(u64 *out, u64 *cell) {
     g = np.arange(n, dtype=np.uint64)
     assert np.array_equal(np.frombuffer(bytes(out), np.uint64), g * g)
     assert int(np.frombuffer(bytes(cell), np.uint64)[0]) == n * (n - 1) // 2
+
+
+def test_device_instruction_counts_match_vgpu(bridge):
+    # every thread's executed IR instructions, summed per region
+    # (HostRunResult.device_instructions, host.py:524-528): the vgpu counts
+    # one per interpreted instruction (vgpu.py:390); the compiled image adds
+    # each basic block's length on entry — equal for every completed launch
+    B.FAST_PATH = False
+    checked = 0
+    for p in GOLDEN["programs"]:
+        if "device_instructions" not in p:
+            continue
+        got = run_source(p["source"], device="b200", **p["kwargs"])
+        assert [list(x) for x in got.device_instructions] == p["device_instructions"], p["name"]
+        checked += 1
+    assert checked >= 15
+
+
+RACE = """
+u32 cell[1];
+u32 seen[64];
+
+void kernel(u32 *cell, u32 *seen) {
+  #pragma omp target num_teams(2) thread_limit(32)
+  {
+    u32 g;
+    g = omp_team_id() * omp_num_threads() + omp_thread_id();
+    seen[g] = __atomic_xchg(cell, g + 1);
+  }
+}
+
+void main() {
+  u32 i;
+  cell[0] = 0;
+  kernel(cell, seen);
+  print(cell[0]);
+  i = 0;
+  while (i < 64) {
+    print(seen[i]);
+    i = i + 1;
+  }
+}
+"""
+
+
+def test_sched_seed_explores_interleavings(bridge):
+    # the vgpu's sched_seed picks an interleaving (vgpu.py:285-306); on the
+    # B200 a nonzero seed jitters every thread before its atomics/barriers,
+    # so different seeds reach the racing xchg chain in different orders.
+    # Every outcome must still be a valid serialisation: the xchg values form
+    # one chain 0 -> g1+1 -> ... through all 64 threads, ending in cell[0].
+    B.FAST_PATH = False
+    finals = set()
+    for seed in range(1, 9):
+        got = run_source(RACE, device="b200", sched_seed=seed)
+        assert got.exit_status == 0 and all(s == 0 for _, s in got.offloads)
+        vals = [int(v) for v in got.stdout.split()]
+        last, seen = vals[0], vals[1:]
+        nxt = {old: g + 1 for g, old in enumerate(seen)}
+        assert len(nxt) == 64  # every old value is distinct: one chain
+        v, hops = 0, 0
+        while v in nxt:
+            v, hops = nxt[v], hops + 1
+        assert hops == 64 and v == last
+        finals.add(last)
+        # the executed-instruction count does not depend on the order
+        assert got.device_instructions == run_source(RACE, device="vgpu").device_instructions
+    assert len(finals) >= 2, finals  # seeds led to different last writers
