@@ -112,11 +112,11 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def lib_sha16() -> str | None:
-    from paper_2106_03219_b200 import _lib
+def src_sha16() -> str:
+    """Fingerprint of the library's sources + build flags (_build.source_sha16)."""
+    from paper_2106_03219_b200 import _build
 
-    p = _lib.lib_path()
-    return hashlib.sha256(p.read_bytes()).hexdigest()[:16] if p.exists() else None
+    return _build.source_sha16()
 
 
 def ncu_capture(teams: int, threads: int, split: int) -> dict:
@@ -133,7 +133,7 @@ def ncu_capture(teams: int, threads: int, split: int) -> dict:
     want = {"kernel": BENCH_KERNEL, "grid": teams * split, "block": threads}
     got = {"kernel": rec.get("kernel", ""), "grid": int(rec.get("launch__grid_size", -1)),
            "block": int(rec.get("launch__block_size", -1))}
-    info = {"captured_at": d.get("captured_at"), "capture_lib_sha16": d.get("lib_sha16"),
+    info = {"captured_at": d.get("captured_at"), "capture_src_sha16": d.get("src_sha16"),
             "capture_kernel": got["kernel"], "capture_grid": got["grid"],
             "capture_block": got["block"]}
     if want["kernel"] not in got["kernel"] or want["grid"] != got["grid"] or \
@@ -141,9 +141,9 @@ def ncu_capture(teams: int, threads: int, split: int) -> dict:
         msg = f"stale ncu capture: captured {got}, timed {want}"
         print(f"bench: WARNING {msg}; roofline.traffic dropped", file=sys.stderr, flush=True)
         return {"status": msg, "traffic": None, "frac_ncu_dram": None, **info}
-    sha = lib_sha16()
-    status = "current" if sha and sha == d.get("lib_sha16") else \
-        f"kernel geometry matches; library rebuilt since the capture (now {sha})"
+    sha = src_sha16()
+    status = "current (captured from these library sources)" if sha == d.get("src_sha16") else \
+        f"kernel geometry matches; library sources changed since the capture (now {sha})"
     return {"status": status, "traffic": d.get("dram_bytes_per_launch"),
             "frac_ncu_dram": round(rec["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
                                    / 100.0, 4), **info}

@@ -7,6 +7,7 @@ cache is used.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -33,8 +34,24 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found: cannot build libomprt_b200.so")
 
 
+# region_rt.cuh is the NVRTC prelude of compiled regions (regionc.py), not
+# part of the library
+NOT_IN_LIB = {"region_rt.cuh"}
+
+
 def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [HEADER]
+    return [p for p in sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [HEADER]
+            if p.name not in NOT_IN_LIB]
+
+
+def source_sha16() -> str:
+    """Fingerprint of what the library is built from (sources + flags): equal
+    for two builds of the same code, unlike the .so's bytes."""
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for p in sources():
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()[:16]
 
 
 def stale() -> bool:
