@@ -148,6 +148,15 @@ int omprt_device_init(int device);
  * bulk-copy path; 2 or 8 force the LDG path. */
 int omprt_set_unroll(int unroll);
 
+/* Tuning knob (not part of the reference interface): CUDA threads per CTA of
+ * the SPMD construct kernels (reduce, axpy_minmax, dot, reduce_exchange) for
+ * this calling thread — 0 (default) = each construct's measured policy; else a
+ * multiple of 32 in 64..1024.  The OpenMP geometry (teams x threads) still
+ * defines every team's iteration set; in SPMD mode which lane of the CTA
+ * folds an iteration is unobservable, so the CTA size is a pure performance
+ * choice. */
+int omprt_set_spmd_block(int threads);
+
 /* Tuning knob (not part of the reference interface): kernel variant used by
  * the fp64 sum in SPMD mode — 0 default; 1-5 LDG load-policy / unroll
  * variants; 10-16 TMA bulk-copy (cp.async.bulk + mbarrier) stage rings;

@@ -58,6 +58,7 @@ _SIGS = {
     "omprt_device_init": ([C.c_int], C.c_int),
     "omprt_set_unroll": ([C.c_int], C.c_int),
     "omprt_set_variant": ([C.c_int], C.c_int),
+    "omprt_set_spmd_block": ([C.c_int], C.c_int),
     "omprt_set_trace": ([C.c_void_p, C.c_int64], C.c_int),
     "omprt_ipc_handle_bytes": ([], C.c_size_t),
     "omprt_mailbox_create": ([C.c_int, C.POINTER(C.c_void_p), C.c_void_p], C.c_int),

@@ -249,6 +249,10 @@ struct LoopArgs {
   int sched;
   int split;    // SPMD: CTAs per OpenMP team (<= 1: one CTA per team)
   int balance;  // SPMD flat chunked: CTAs take balanced contiguous pieces
+  int threads;  // OpenMP threads per team (0: blockDim.x).  SPMD kernels may
+                // run a team on a CTA of another size: the team's iteration
+                // set depends on the OpenMP geometry only, which lane of the
+                // CTA folds an iteration is unobservable
 };
 
 // Contiguous piece k of `cl` of [first, end): cut points on absolute
@@ -301,7 +305,8 @@ OMPRT_D TeamSet team_set_cta(const LoopArgs &la) {
     contiguous_piece(s, la.lb, la.ub + 1, blockIdx.x, gridDim.x);
     return s;
   }
-  TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, team, teams, blockDim.x);
+  TeamSet s = team_set(la.sched, la.lb, la.ub, la.chunk, team, teams,
+                       la.threads > 0 ? la.threads : (int64_t)blockDim.x);
   if (cl == 1 || s.nseg <= 0) return s;
   if (s.seg_stride == 0 || s.nseg <= 1) {
     int64_t len = s.ub - s.first + 1;

@@ -82,6 +82,7 @@ class DeviceGuard {
 // changes the kernel another caller's launch selects.
 thread_local int g_unroll = 4;   // vectors in flight per lane per iteration
 thread_local int g_variant = 0;  // kernel variant of the fp64 sum (0 = default)
+thread_local int g_spmd_block = 0;  // CUDA threads per SPMD CTA (0 = the policy below)
 constexpr int kOrderedLiteral = 20;  // variant: ORDERED mode through the literal walk
 bool g_trace_on = false;  // a trace ring is installed (selects traced kernel instances)
 
@@ -198,6 +199,25 @@ int spmd_split(int teams) {
 void spmd_prepare(LoopArgs &la, int teams) {
   la.split = spmd_split(teams);
   la.balance = g_variant == kNoSplit ? 0 : 1;
+}
+
+// CUDA threads per CTA of an SPMD construct kernel running an OpenMP team of
+// `threads` (LoopArgs::threads carries the OpenMP count): the tuning knob if
+// set, else `pref` (the construct's measured best), else the OpenMP count
+// rounded up to a whole number of warps (at least two: producer + consumer).
+// Preferred CTA sizes per construct (0: follow the OpenMP thread count),
+// measured with the OpenMP geometry fixed (profiles/r2_block_sweep.jsonl):
+// the fp64 sum at 2^30 streams best from 384-thread CTAs whatever the team
+// size (OpenMP 148 x 1024: 5.97 TB/s on 1024-thread CTAs, 7.05 on 384), the
+// two-stream dot from 256 (7.09-7.13 vs 6.94 at 384); axpy (read, read,
+// write) from 1024 (+1-3 % over 256-768: more warps issue the y stores).
+constexpr int kReduceBlock = 384, kAxpyBlock = 1024, kDotBlock = 256;
+
+int spmd_block(int threads, int pref) {
+  if (g_spmd_block > 0) return g_spmd_block;
+  if (pref > 0) return pref;
+  int b = (threads + 31) / 32 * 32;
+  return b < 64 ? 64 : b;
 }
 
 // ORDERED row-group kernels (ordered.cuh).  Each CTA = nw streaming warps +
@@ -333,7 +353,6 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
     if (g_variant != 0 && g_variant < kOrderedLiteral && mode == OMPRT_MODE_SPMD)
       return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
   }
-  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
   // Integer add (mod 2^n), max and min are associative and commutative: the
   // reference order's result IS the re-associated one, bit for bit, so
   // ORDERED integer reductions take the SPMD kernels (variant kOrderedLiteral
@@ -356,16 +375,16 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
     }
   } else {
     spmd_prepare(la, teams);
+    la.threads = threads;
     const int grid = teams * la.split;
-    if (bulk_ok) {
+    const int blk = spmd_block(threads, kReduceBlock);
+    if (g_unroll == 4) {
       // default SPMD path: TMA bulk-copy stage ring
-      return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, threads, w, op, st);
+      return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, blk, w, op, st);
     } else if (g_unroll >= 8) {
-      k_reduce<T, OP, 8><<<grid, threads, 0, st>>>(xp, la, w, op);
-    } else if (g_unroll <= 2) {
-      k_reduce<T, OP, 2><<<grid, threads, 0, st>>>(xp, la, w, op);
+      k_reduce<T, OP, 8><<<grid, blk, 0, st>>>(xp, la, w, op);
     } else {
-      k_reduce<T, OP, 4><<<grid, threads, 0, st>>>(xp, la, w, op);
+      k_reduce<T, OP, 2><<<grid, blk, 0, st>>>(xp, la, w, op);
     }
   }
   return check_launch("omprt_reduce");
@@ -432,7 +451,9 @@ int launch_exchange_t(const void *x, LoopArgs la, int teams, int threads, Worksp
   int rc = set_smem(kern, smem);
   if (rc) return rc;
   spmd_prepare(la, teams);
-  kern<<<teams * la.split, threads, smem, st>>>((const T *)x, la, w, (T *)out, xc);
+  la.threads = threads;
+  kern<<<teams * la.split, spmd_block(threads, kReduceBlock), smem, st>>>((const T *)x, la, w,
+                                                                          (T *)out, xc);
   return check_launch("omprt_reduce_exchange");
 }
 
@@ -803,6 +824,14 @@ int omprt_set_unroll(int unroll) {
   return OMPRT_OK;
 }
 
+int omprt_set_spmd_block(int threads) {
+  if (threads != 0 && (threads < 64 || threads > 1024 || threads % 32 != 0))
+    return fail(OMPRT_EINVAL, "SPMD block must be 0 or a multiple of 32 in 64..1024 (got %d)",
+                threads);
+  g_spmd_block = threads;
+  return OMPRT_OK;
+}
+
 int omprt_set_variant(int variant) {
   if (variant < 0) return fail(OMPRT_EINVAL, "variant must be >= 0");
   g_variant = variant;
@@ -856,16 +885,17 @@ namespace {
 int launch_axpy_spmd(float a, const float *d_x, float *d_y, LoopArgs la, int teams, int threads,
                      Workspace w, float *d_max, float *d_min, cudaStream_t st) {
   int rc;
-  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
   spmd_prepare(la, teams);
-  if (bulk_ok) {
-    auto kern = threads <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
-                               : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
+  la.threads = threads;
+  const int blk = spmd_block(threads, kAxpyBlock);
+  if (g_unroll == 4) {
+    auto kern = blk <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
+                           : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
     if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams * la.split, threads, smem, st>>>(a, d_x, d_y, la, w, d_max, d_min);
+    kern<<<teams * la.split, blk, smem, st>>>(a, d_x, d_y, la, w, d_max, d_min);
   } else {
-    k_axpy_minmax<4><<<teams * la.split, threads, 0, st>>>(a, d_x, d_y, la, w, d_max, d_min);
+    k_axpy_minmax<4><<<teams * la.split, blk, 0, st>>>(a, d_x, d_y, la, w, d_max, d_min);
   }
   return check_launch("omprt_axpy_minmax");
 }
@@ -928,7 +958,6 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
     return fail(OMPRT_EINVAL, "dot: null device pointer");
   LoopArgs la{lb, ub, chunk, sched};
   Workspace w = ws_carve(d_ws, teams, 2);
-  const bool bulk_ok = threads >= 64 && threads % 32 == 0 && g_unroll == 4;
   if (mode == OMPRT_MODE_ORDERED) {
     if (g_variant != kOrderedLiteral && ord_rows_ok(la, d_x, d_y)) {
       // six warps when they fill whole waves: two streams' 256-byte windows
@@ -967,18 +996,20 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
     } else {
       k_dot_ordered<<<teams, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
     }
-  } else if (bulk_ok) {
-    spmd_prepare(la, teams);
-    auto kern = k_dot_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
-    const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
-    if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams * la.split, threads, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
   } else {
     spmd_prepare(la, teams);
-    if (g_unroll >= 8)
-      k_dot<8><<<teams * la.split, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
-    else
-      k_dot<4><<<teams * la.split, threads, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+    la.threads = threads;
+    const int blk = spmd_block(threads, kDotBlock);
+    if (g_unroll == 4) {
+      auto kern = k_dot_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
+      const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
+      if ((rc = set_smem(kern, smem))) return rc;
+      kern<<<teams * la.split, blk, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
+    } else if (g_unroll >= 8) {
+      k_dot<8><<<teams * la.split, blk, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+    } else {
+      k_dot<4><<<teams * la.split, blk, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
+    }
   }
   return check_launch("omprt_dot");
 }

@@ -114,6 +114,12 @@ def set_unroll(unroll: int) -> None:
     check(_lib.load().omprt_set_unroll(unroll), "omprt_set_unroll")
 
 
+def set_spmd_block(threads: int) -> None:
+    """Tuning: CUDA threads per CTA of the SPMD construct kernels for this
+    thread (0 = the measured per-construct policy; see omprt_set_spmd_block)."""
+    check(_lib.load().omprt_set_spmd_block(threads), "omprt_set_spmd_block")
+
+
 def set_variant(variant: int) -> None:
     """Tuning: kernel variant of the fp64 sum (see omprt_set_variant)."""
     check(_lib.load().omprt_set_variant(variant), "omprt_set_variant")

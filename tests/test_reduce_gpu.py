@@ -275,3 +275,39 @@ def test_team_split_matches_one_cta_per_team(cuda, sched):
             assert abs(gf - ex) <= 1e-6 * ex
     finally:
         runtime.set_variant(0)
+
+
+def test_spmd_cta_size_is_unobservable(cuda):
+    # the OpenMP geometry defines every team's iteration set; the CTA that
+    # runs a team may have another size (omprt_set_spmd_block): integer
+    # results are identical for every CTA size, also for OpenMP thread
+    # counts that are not a multiple of 32
+    n = 1_000_003
+    x = O.fill(n, O.I64, O.SEED, 13)
+    xd = torch.from_numpy(x).to(cuda)
+    try:
+        for sched in SCHEDS:
+            for teams, threads, chunk in ((148, 384, 64), (37, 100, 7), (3, 1000, 4096)):
+                want = int(O.reduce(x, 0, n - 1, O.I64, O.ADD, SCHEDS[sched], chunk, teams,
+                                    threads, 0))
+                for blk in (0, 64, 96, 384, 1024):
+                    runtime.set_spmd_block(blk)
+                    got = run_reduce(cuda, x, O.I64, "add", sched, chunk, teams, threads, 0, n - 1)
+                    assert int(got) == want, (sched, teams, threads, chunk, blk)
+    finally:
+        runtime.set_spmd_block(0)
+    # axpy + max/min: y bit for bit, max/min exact
+    xf = O.fill(n, O.F32, O.SEED, 0)
+    yf = O.fill(n, O.F32, O.SEED, 1)
+    yo = yf.copy()
+    mx, mn = O.axpy_minmax(1.5, xf, yo, 0, n - 1, O.STATIC_CHUNKED, 64, 37, 100, -np.inf, np.inf)
+    try:
+        for blk in (64, 1024):
+            runtime.set_spmd_block(blk)
+            xd2, yd2 = torch.from_numpy(xf).to(cuda), torch.from_numpy(yf).to(cuda)
+            gmx, gmn = runtime.axpy_minmax(1.5, xd2, yd2, sched="static_chunked", chunk=64,
+                                           teams=37, threads=100)
+            assert np.array_equal(yd2.cpu().numpy(), yo) and float(gmx.item()) == mx \
+                and float(gmn.item()) == mn
+    finally:
+        runtime.set_spmd_block(0)
