@@ -382,7 +382,11 @@ int omprt_fill(void *d_x, int64_t n, int dtype, uint64_t seed, int k, int64_t of
  * memory) to a device buffer, omprt_reduce over [0, n-1], copy-out of the
  * scalar result into *h_out (which holds the initial value on entry), only on
  * status 0.  Synchronous.  The device buffers are cached across calls, per
- * CUDA device (the calling thread's current device runs the region). */
+ * CUDA device (the calling thread's current device runs the region).  Above
+ * 512 MiB an SPMD (or integer) reduction is pipelined: the input lands in
+ * 256 MiB pieces on a copy stream while the previous piece is reduced, each
+ * piece's launch accumulating into the cell (integers bit-exact, fp within
+ * the SPMD tolerance); ORDERED fp copies everything first. */
 int omprt_reduce_host(const void *h_x, int64_t n, int dtype, int op, int sched,
                       int64_t chunk, int teams, int threads, int mode, void *h_out);
 

@@ -599,6 +599,13 @@ size_t generic_ws_core(int teams) { return ws_bytes(teams, 0, OMPRT_MODE_SPMD, 1
 // Host-buffer (tgt_target-shaped) entries: device staging cached per CUDA
 // device (a buffer belongs to the context it was allocated in, so a caller
 // that switches devices gets that device's own staging, never another's).
+// reduce_host pipelining: the input lands in pieces of kHostPipeBytes on a
+// copy stream while the reduction of the previous piece runs on the compute
+// stream (SPMD: the construct accumulates into the cell, so piecewise
+// launches give the same integers and a re-associated fp sum).
+constexpr size_t kHostPipeBytes = (size_t)256 << 20;
+constexpr int kHostPipeEvents = 4;
+
 struct HostStaging {
   void *buf[2] = {nullptr, nullptr};  // input / in-out arrays
   size_t bytes[2] = {0, 0};
@@ -608,6 +615,8 @@ struct HostStaging {
   int64_t *offs = nullptr;            // generic mode: per-team arena offsets
   size_t offs_bytes = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;        // copy-in stream of the pipelined reduce_host
+  cudaEvent_t landed[kHostPipeEvents] = {};
 };
 std::mutex g_host_mu;
 std::unordered_map<int, HostStaging> g_host;
@@ -634,6 +643,11 @@ int staging(HostStaging *&out, size_t b0, size_t b1, size_t ws) {
   OMPRT_CUDA(cudaGetDevice(&dev));
   HostStaging &h = g_host[dev];
   if (!h.stream) OMPRT_CUDA(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+  if (!h.copy) {
+    OMPRT_CUDA(cudaStreamCreateWithFlags(&h.copy, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : h.landed)
+      OMPRT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   int rc;
   if ((rc = staging_grow(h.buf[0], h.bytes[0], b0, false)) ||
       (rc = staging_grow(h.buf[1], h.bytes[1], b1, false)) ||
@@ -1190,11 +1204,35 @@ int omprt_reduce_host(const void *h_x, int64_t n, int dtype, int op, int sched, 
   if ((rc = staging(h, xbytes, 0, omprt_reduce_workspace_bytes(teams, threads, mode)))) return rc;
   cudaStream_t st = h->stream;
   // copy-in (tgt_target host.py:276-281)
-  if (xbytes) OMPRT_CUDA(cudaMemcpyAsync(h->buf[0], h_x, xbytes, cudaMemcpyHostToDevice, st));
   OMPRT_CUDA(cudaMemcpyAsync(h->cells, h_out, es, cudaMemcpyHostToDevice, st));
-  rc = omprt_reduce(h->buf[0], 0, n - 1, dtype, op, sched, chunk, teams, threads, mode, h->ws,
-                    h->cells, st);
-  if (rc) return rc;
+  const bool pipe = xbytes > 2 * kHostPipeBytes &&
+                    (mode == OMPRT_MODE_SPMD || dtype == OMPRT_I32 || dtype == OMPRT_U32 ||
+                     dtype == OMPRT_I64 || dtype == OMPRT_U64);
+  if (!pipe) {
+    if (xbytes) OMPRT_CUDA(cudaMemcpyAsync(h->buf[0], h_x, xbytes, cudaMemcpyHostToDevice, st));
+    rc = omprt_reduce(h->buf[0], 0, n - 1, dtype, op, sched, chunk, teams, threads, mode, h->ws,
+                      h->cells, st);
+    if (rc) return rc;
+  } else {
+    // piece k lands on the copy stream while piece k-1 is reduced on st;
+    // every piece's construct launch accumulates into the cell
+    const int64_t per = (int64_t)(kHostPipeBytes / es);
+    OMPRT_CUDA(cudaEventRecord(h->landed[0], st));  // the copy stream starts after the cell
+    OMPRT_CUDA(cudaStreamWaitEvent(h->copy, h->landed[0], 0));
+    int k = 0;
+    for (int64_t lo = 0; lo < n; lo += per, ++k) {
+      const int64_t cnt = n - lo < per ? n - lo : per;
+      unsigned char *dst = static_cast<unsigned char *>(h->buf[0]) + (size_t)lo * es;
+      OMPRT_CUDA(cudaMemcpyAsync(dst, static_cast<const unsigned char *>(h_x) + (size_t)lo * es,
+                                 (size_t)cnt * es, cudaMemcpyHostToDevice, h->copy));
+      cudaEvent_t ev = h->landed[k % kHostPipeEvents];
+      OMPRT_CUDA(cudaEventRecord(ev, h->copy));
+      OMPRT_CUDA(cudaStreamWaitEvent(st, ev, 0));
+      rc = omprt_reduce(dst, 0, cnt - 1, dtype, op, sched, chunk, teams, threads, mode, h->ws,
+                        h->cells, st);
+      if (rc) return rc;
+    }
+  }
   // copy-out only on status 0 (host.py:293-295)
   unsigned char res[16];
   OMPRT_CUDA(cudaMemcpyAsync(res, h->cells, es, cudaMemcpyDeviceToHost, st));
@@ -1318,6 +1356,9 @@ int omprt_release_host_cache(void) {
     for (void *p : {h.buf[0], h.buf[1], h.ws, h.cells, static_cast<void *>(h.offs)})
       if (p) cudaFree(p);
     if (h.stream) cudaStreamDestroy(h.stream);
+    if (h.copy) cudaStreamDestroy(h.copy);
+    for (cudaEvent_t e : h.landed)
+      if (e) cudaEventDestroy(e);
   }
   g_host.clear();
   if (prev >= 0) cudaSetDevice(prev);

@@ -148,6 +148,27 @@ def test_reduce_host_entry(cuda):
     assert c2[0] == O.reduce(xn, 0, n - 1, O.F64, O.ADD, O.STATIC, 1, 148, 256)
 
 
+def test_reduce_host_pipelined(cuda):
+    # above 512 MiB the input lands in 256 MiB pieces on a copy stream while
+    # the previous piece is reduced (each launch accumulates into the cell):
+    # integers bit-exact, fp64 SPMD within 1e-6; a ragged last piece
+    n = (600 << 20) // 8 + 12345
+    x = torch.from_numpy(O.fill(n, O.I64, O.SEED, 8)).pin_memory()
+    cell = torch.tensor([-3], dtype=torch.int64)
+    reduce_host(x, cell, sched="distribute", teams=148, threads=384)
+    assert int(cell.item()) == O._signed(-3 + int(O.reduce_flat_gen(0, n - 1, O.I64, O.ADD, k=8)),
+                                         64)
+    cmax = torch.tensor([-(1 << 63)], dtype=torch.int64)
+    reduce_host(x, cmax, op="max", teams=148, threads=384, mode="ordered")
+    assert int(cmax.item()) == int(x.max().item())
+    xf = torch.from_numpy(O.fill(n, O.F64, O.SEED, 8)).pin_memory()
+    cf = torch.zeros(1, dtype=torch.float64)
+    reduce_host(xf, cf, sched="distribute", teams=148, threads=384)
+    ex = O.exact_sum_gen(0, n - 1, O.F64, k=8)
+    assert abs(float(cf.item()) - ex) <= 1e-6 * ex
+    del x, xf
+
+
 def test_axpy_dot_generic_host_entries(cuda):
     """The host-buffer C entries for configs 3, 5 and 4: copy-in, launch,
     copy-out only on status 0 (host.py:276-295), bit-exact vs the oracle."""

@@ -1,8 +1,9 @@
 """Randomised bit-exactness fuzz of every ORDERED path against the oracle's
 reference order: fp32/fp64 sums and max/min (row-group kernels with static
 and dynamic segments, literal walk), fp64 dot, axpy + max/min; plus SPMD
-integer reductions (bit-exact: every bulk / LDG / team-split path) and SPMD
-fp64 sums (within 1e-6 of the exact sum).  Sizes are
+integer reductions (bit-exact: every bulk / LDG / team-split path), SPMD
+fp64 sums and dots (within 1e-6) and SPMD axpy + max/min (y bit-exact,
+max/min exact) at random CTA sizes (omprt_set_spmd_block).  Sizes are
 chosen so that rows span many windows (dynamic segments > 1) as well as
 single windows.  Prints one JSON summary line; exits 1 on any mismatch.
 
@@ -48,9 +49,31 @@ def main():
         lb = int(rng.integers(0, 100))
         ub = int(rng.integers(lb - 2, N))
         kind = str(rng.choice(["sum64", "sum32", "max64", "min32", "dot", "axpy",
-                               "spmd_i64", "spmd_u32max", "spmd_f64"]))
+                               "spmd_i64", "spmd_u32max", "spmd_f64", "spmd_dot", "spmd_axpy"]))
         kinds[kind] = kinds.get(kind, 0) + 1
-        if kind.startswith("spmd"):
+        # SPMD kinds also draw the CTA size (omprt_set_spmd_block; 0 = policy)
+        blk = int(rng.choice([0, 0, 0, 64, 96, 256, 384, 1024])) if kind.startswith("spmd") else 0
+        runtime.set_spmd_block(blk)
+        if kind == "spmd_dot":
+            want = O.dot(data[O.F64], y64, lb, ub, SCHEDS[sched], chunk, teams, threads)
+            got = float(runtime.dot(dev_data[O.F64], y64d, lb=lb, ub=ub, sched=sched, chunk=chunk,
+                                    teams=teams, threads=threads).item())
+            ok = abs(got - want) <= 1e-6 * max(abs(want), 1e-30)
+        elif kind == "spmd_axpy":
+            n = min(N, 2_000_003)
+            ub = min(ub, n - 1)
+            x = data[O.F32][:n]
+            y = O.fill(n, O.F32, O.SEED, 7)
+            yo = y.copy()
+            mx, mn = O.axpy_minmax(0.75, x, yo, lb, ub, SCHEDS[sched], chunk, teams, threads,
+                                   -np.inf, np.inf)
+            yd = torch.from_numpy(y).to(dev)
+            gmx, gmn = runtime.axpy_minmax(0.75, dev_data[O.F32][:n], yd, lb=lb, ub=ub,
+                                           sched=sched, chunk=chunk, teams=teams,
+                                           threads=threads)
+            ok = (float(gmx.item()) == float(mx) and float(gmn.item()) == float(mn)
+                  and np.array_equal(yd.cpu().numpy().view(np.uint32), yo.view(np.uint32)))
+        elif kind.startswith("spmd"):
             dt, op = {"spmd_i64": (O.I64, "add"), "spmd_u32max": (O.U32, "max"),
                       "spmd_f64": (O.F64, "add")}[kind]
             init = 0
@@ -96,9 +119,10 @@ def main():
             ok = (np.float32(gmx.item()).tobytes() == np.float32(mx).tobytes()
                   and np.float32(gmn.item()).tobytes() == np.float32(mn).tobytes()
                   and np.array_equal(yd.cpu().numpy().view(np.uint32), yo.view(np.uint32)))
+        runtime.set_spmd_block(0)
         if not ok:
             fails.append({"case": c, "kind": kind, "sched": sched, "chunk": chunk,
-                          "teams": teams, "threads": threads, "lb": lb, "ub": ub})
+                          "teams": teams, "threads": threads, "lb": lb, "ub": ub, "cta": blk})
     print(json.dumps({"cases": a.cases, "kinds": kinds, "failures": len(fails),
                       "first_failures": fails[:5]}), flush=True)
     sys.exit(1 if fails else 0)
