@@ -57,16 +57,23 @@ OMPRT_D void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
       : "memory");
 }
 
-// Default ring: 4 x 32 KiB = 128 KiB in flight per team, one team per SM.
-// Measured steady state (power-capped, back to back) on B200: a 256-thread
-// team streams as fast as a 1024-thread one in isolation but draws less
-// power, so it keeps ~7.46 TB/s where 1024 threads settle at ~7.13 TB/s
-// (profiles/r1_steady_bulk.jsonl).
-constexpr int kBulkStages = 4;
-constexpr int kBulkStageBytes = 32768;
-// Two-stream rings (dot, axpy): 4 stages x 2 streams x 16 KiB = 128 KiB.
+// Default ring: 2 x 96 KiB = 192 KiB in flight per team, one team per SM.
+// Steady state (power-capped, back to back, same process, alternating
+// blocks): 2 x 96 KiB 7.34-7.36 TB/s vs round 1's 4 x 32 KiB 7.17-7.21;
+// 3 x 64 KiB 7.23-7.33, 2 x 112 KiB 7.18, 4 x 48 KiB 7.17, 3 x 72 KiB 7.04,
+// 2 x 64 KiB 7.02, 4 x 56 KiB 6.83 (profiles/r2_ring_steady_*.jsonl):
+// big stages mean few mbarrier round trips per byte, two of them keep one
+// landing while the other is folded.  (Round 1: a 256-thread team streams as
+// fast as a 1024-thread one in isolation but draws less power,
+// profiles/r1_steady_bulk.jsonl.)
+constexpr int kBulkStages = 2;
+constexpr int kBulkStageBytes = 98304;
+// Two-stream rings: axpy 4 stages x 2 streams x 16 KiB = 128 KiB (bigger
+// stages lose 3-4 %: its consumers also store y); dot 2 x 2 x 48 KiB.
 constexpr int kBulk2Stages = 4;
 constexpr int kBulk2StageBytes = 16384;
+constexpr int kDotStages = 2;
+constexpr int kDotStageBytes = 49152;
 
 template <int STAGES, int STAGE_BYTES> struct BulkSmem {
   static constexpr size_t bytes = (size_t)STAGES * STAGE_BYTES;

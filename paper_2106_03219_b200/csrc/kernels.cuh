@@ -249,6 +249,7 @@ struct LoopArgs {
   int sched;
   int split;    // SPMD: CTAs per OpenMP team (<= 1: one CTA per team)
   int balance;  // SPMD flat chunked: CTAs take balanced contiguous pieces
+  int64_t tile;  // balance == 2 (tuning): CTAs take interleaved tiles of `tile` elements
   int threads;  // OpenMP threads per team (0: blockDim.x).  SPMD kernels may
                 // run a team on a CTA of another size: the team's iteration
                 // set depends on the OpenMP geometry only, which lane of the
@@ -288,6 +289,16 @@ OMPRT_D void contiguous_piece(TeamSet &s, int64_t first, int64_t end, int64_t k,
 OMPRT_D TeamSet team_set_cta(const LoopArgs &la) {
   const int64_t cl = la.split > 1 ? la.split : 1;
   const int64_t teams = gridDim.x / cl, team = blockIdx.x / cl, sub = blockIdx.x % cl;
+  if (la.balance == 2) {
+    // tuning variant: CTA b takes tiles b, b + G, b + 2G, ... of [lb, ub]
+    TeamSet s;
+    s.ub = la.ub;
+    s.first = la.lb + (int64_t)blockIdx.x * la.tile;
+    s.seg_len = la.tile;
+    s.seg_stride = (int64_t)gridDim.x * la.tile;
+    s.nseg = (la.ub >= s.first) ? (la.ub - s.first) / s.seg_stride + 1 : 0;
+    return s;
+  }
   if (la.balance && la.sched == OMPRT_SCHED_STATIC_CHUNKED) {
     // The flat chunked teeth of all teams tile [lb, ub] exactly once, so the
     // union is contiguous: every CTA takes an equal contiguous piece of it

@@ -163,6 +163,21 @@ int launch_variant(int v, const T *xp, LoopArgs la, int teams, int threads, Work
     case 15: if (bulk_ok) return launch_bulk<T, OP, 2, 32768>(xp, la, teams, threads, w, op, st); break;
     case 16: if (bulk_ok) return launch_bulk<T, OP, 12, 8192>(xp, la, teams, threads, w, op, st); break;
     case 17: if (bulk_ok) return launch_bulk<T, OP, 4, 32768, true>(xp, la, teams, threads, w, op, st); break;
+    case 18: if (bulk_ok) return launch_bulk<T, OP, 6, 32768>(xp, la, teams, threads, w, op, st); break;
+    case 19: if (bulk_ok) return launch_bulk<T, OP, 3, 65536>(xp, la, teams, threads, w, op, st); break;
+    case 36: if (bulk_ok) return launch_bulk<T, OP, 4, 49152>(xp, la, teams, threads, w, op, st); break;
+    case 37: if (bulk_ok) return launch_bulk<T, OP, 2, 98304>(xp, la, teams, threads, w, op, st); break;
+    case 38: if (bulk_ok) return launch_bulk<T, OP, 2, 65536>(xp, la, teams, threads, w, op, st); break;
+    case 39: if (bulk_ok) return launch_bulk<T, OP, 2, 114688>(xp, la, teams, threads, w, op, st); break;
+    case 40: if (bulk_ok) return launch_bulk<T, OP, 3, 73728>(xp, la, teams, threads, w, op, st); break;
+    case 46: if (bulk_ok) return launch_bulk<T, OP, 4, 57344>(xp, la, teams, threads, w, op, st); break;
+    // interleaved CTA tiles of 64 KiB / 512 KiB / 2 MiB (every CTA streams
+    // neighbouring addresses at the same time) on the default ring
+    case 33: case 34: case 35:
+      if (!bulk_ok) break;
+      la.balance = 2;
+      la.tile = (int64_t)(v == 33 ? 65536 : v == 34 ? 524288 : 2097152) / (int64_t)sizeof(T);
+      return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, threads, w, op, st);
     default: return fail(OMPRT_EINVAL, "unknown variant %d", v);
   }
   if (v >= 10) k_reduce<T, OP, 4><<<teams, threads, 0, st>>>(xp, la, w, op);
@@ -350,7 +365,8 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
   const T *xp = (const T *)x;
   T *op = (T *)out;
   if constexpr (std::is_same<T, double>::value && OP == OMPRT_OP_ADD) {
-    if (g_variant != 0 && g_variant < kOrderedLiteral && mode == OMPRT_MODE_SPMD)
+    if (g_variant != 0 && mode == OMPRT_MODE_SPMD &&
+        (g_variant < kOrderedLiteral || (g_variant >= 33 && g_variant <= 40) || g_variant == 46))
       return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
   }
   // Integer add (mod 2^n), max and min are associative and commutative: the
@@ -902,7 +918,13 @@ int launch_axpy_spmd(float a, const float *d_x, float *d_y, LoopArgs la, int tea
   spmd_prepare(la, teams);
   la.threads = threads;
   const int blk = spmd_block(threads, kAxpyBlock);
-  if (g_unroll == 4) {
+  if (g_unroll == 4 && (g_variant == 47 || g_variant == 48)) {
+    // tuning: two-stream rings 2 x 2 x 48 KiB (47) / 3 x 2 x 32 KiB (48)
+    auto kern = g_variant == 47 ? k_axpy_minmax_bulk<2, 49152, 4> : k_axpy_minmax_bulk<3, 32768, 4>;
+    const size_t smem = g_variant == 47 ? (size_t)2 * 2 * 49152 : (size_t)2 * 3 * 32768;
+    if ((rc = set_smem(kern, smem))) return rc;
+    kern<<<teams * la.split, blk, smem, st>>>(a, d_x, d_y, la, w, d_max, d_min);
+  } else if (g_unroll == 4) {
     auto kern = blk <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
                            : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
@@ -1014,9 +1036,17 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
     spmd_prepare(la, teams);
     la.threads = threads;
     const int blk = spmd_block(threads, kDotBlock);
-    if (g_unroll == 4) {
-      auto kern = k_dot_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
-      const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
+    if (g_unroll == 4 && g_variant == 48) {
+      // tuning: 3 stages x 2 streams x 32 KiB
+      auto kern = k_dot_bulk<3, 32768, 4>;
+      const size_t smem = (size_t)2 * 3 * 32768;
+      if ((rc = set_smem(kern, smem))) return rc;
+      kern<<<teams * la.split, blk, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
+    } else if (g_unroll == 4) {
+      // 2 stages x 2 streams x 48 KiB (7.50 vs 7.42 TB/s for 4 x 2 x 16 KiB,
+      // steady state, profiles/r2_ring2_steady.jsonl)
+      auto kern = k_dot_bulk<kDotStages, kDotStageBytes, 4>;
+      const size_t smem = (size_t)2 * kDotStages * kDotStageBytes;
       if ((rc = set_smem(kern, smem))) return rc;
       kern<<<teams * la.split, blk, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
     } else if (g_unroll >= 8) {
