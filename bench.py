@@ -446,6 +446,33 @@ def kernel_ms(launch, reps: int, stream, G: int, dev) -> float:
     return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / reps, G, dev)
 
 
+def bind_numa(index: int) -> dict:
+    """Pin this rank's host threads to the NUMA node its GPU hangs off (sysfs
+    numa_node of the GPU's PCI function), so the pinned e2e buffer it
+    allocates next is node-local and the copy-in does not cross the socket
+    interconnect.  N > 1 only: at N = 1 the CPU-baseline leg keeps every core."""
+    import torch
+
+    p = torch.cuda.get_device_properties(index)
+    bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    info = {"gpu_pci": bdf, "numa_node": None, "cpus": None}
+    try:
+        node = int(Path(f"/sys/bus/pci/devices/{bdf}/numa_node").read_text())
+        if node < 0:
+            return info
+        cpus = set()
+        for part in Path(f"/sys/devices/system/node/node{node}/cpulist").read_text().split(","):
+            a, _, b = part.strip().partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            info.update(numa_node=node, cpus=len(cpus))
+    except (OSError, ValueError):
+        pass
+    return info
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -458,6 +485,7 @@ def run_ours(args) -> None:
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    numa = bind_numa(local) if world > 1 else None
     if world > 1:
         if args.backend == "nccl":
             # NCCL's INIT log (rank count, NVLS/P2P transport) stays reachable,
@@ -595,6 +623,7 @@ def run_ours(args) -> None:
                "path": "omprt_reduce_host (C ABI, pinned host buffer, copy-in + reduce + "
                        "copy-out per step), all ranks at once",
                "elements_per_rank": n_e2e,
+               "host_numa": numa,
                "bound": "PCIe host->device copy of the 8 GiB input (Gen5 x16, 64 GB/s raw "
                         "per GPU)"}
         del hx
