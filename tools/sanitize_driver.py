@@ -62,6 +62,19 @@ with runtime.Trace(dev):
 runtime.set_unroll(8)
 runtime.reduce(x, teams=8, threads=256)
 runtime.set_unroll(4)
+# round 2: SPMD construct CTAs decoupled from the OpenMP team size (odd sizes,
+# per-thread override), balanced flat chunked pieces, the C3 ORDERED max/min
+# group trees at 1024-thread teams, the 2 x 96 KiB bench ring geometry
+runtime.reduce(x, sched="static_chunked", chunk=4096, teams=148, threads=1024)
+runtime.reduce(x, sched="distribute", teams=148, threads=384)
+runtime.set_spmd_block(160)
+runtime.reduce(x, sched="static", teams=9, threads=1000)
+runtime.dot(x, x, sched="static_chunked", chunk=1, teams=7, threads=300)
+runtime.axpy_minmax(0.5, xf, yf, sched="static_chunked", chunk=64, teams=5, threads=96)
+runtime.set_spmd_block(0)
+runtime.axpy_minmax(0.5, xf, yf, sched="distribute", teams=148, threads=1024, mode="ordered")
+runtime.generic_reduce(x, teams=64, par_threads=256)
+runtime.generic_reduce(x, teams=64, par_threads=256, ordered=True)
 runtime.bounds_dump(0, 99_999, "static_chunked", 3, teams=4, threads=64, device=dev)
 runtime.generic_reduce(xi, teams=16, par_threads=64)
 runtime.generic_reduce(xi, teams=16, par_threads=64, ordered=True)
