@@ -48,7 +48,7 @@ METRIC = "reduction GB/s (frac of HBM peak) at N=2^30, 1/2/4/8 B200 vs CPU ref"
 N_PER_GPU = 1 << 30
 ELEM = 8  # fp64
 SEED = 0x210603219
-BENCH_KERNEL = "k_reduce_bulk<double, 0, 2, 98304, 0>"
+BENCH_KERNEL = "k_reduce_bulk<double, 0, 3, 49152, 0>"
 
 
 def parse():
@@ -717,7 +717,7 @@ def run_ours(args) -> None:
                          "peak_source": pk["source"] + "; a read+write copy, so a read-only "
                                         "kernel can exceed 1.0 — frac_ncu_dram is ncu's "
                                         "DRAM-throughput fraction of this kernel",
-                         "kernel": "omprt::k_reduce_bulk<double,ADD,2,98304> (TMA bulk-copy ring, 2 x 96 KiB stages)",
+                         "kernel": "omprt::k_reduce_bulk<double,ADD,3,49152> (TMA bulk-copy ring, 3 x 48 KiB stages)",
                          "kernel_avg_ms": round(k_avg_ms, 5),
                          "read_calibration": {"gbs": round(cal_gbs, 1),
                                               "what": "torch.sum over the same 8 GiB, best of 5",

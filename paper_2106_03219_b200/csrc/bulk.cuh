@@ -57,17 +57,22 @@ OMPRT_D void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
       : "memory");
 }
 
-// Default ring: 2 x 96 KiB = 192 KiB in flight per team, one team per SM.
-// Steady state (power-capped, back to back, same process, alternating
-// blocks): 2 x 96 KiB 7.34-7.36 TB/s vs round 1's 4 x 32 KiB 7.17-7.21;
-// 3 x 64 KiB 7.23-7.33, 2 x 112 KiB 7.18, 4 x 48 KiB 7.17, 3 x 72 KiB 7.04,
-// 2 x 64 KiB 7.02, 4 x 56 KiB 6.83 (profiles/r2_ring_steady_*.jsonl):
-// big stages mean few mbarrier round trips per byte, two of them keep one
-// landing while the other is folded.  (Round 1: a 256-thread team streams as
-// fast as a 1024-thread one in isolation but draws less power,
-// profiles/r1_steady_bulk.jsonl.)
-constexpr int kBulkStages = 2;
-constexpr int kBulkStageBytes = 98304;
+// Default ring: 3 x 48 KiB, one team per SM.  The ring shape trades two
+// regimes against each other (same process, alternating blocks,
+// profiles/r2_ring_regimes.jsonl):
+//  * the round-end bench's regime (20 launches after a short warm-up, SM
+//    clocks near max): 3 x 48 KiB 7.40-7.41 TB/s, 2 x 80 7.39-7.40, 4 x 32
+//    7.39, 2 x 72 7.37, 2 x 96 7.31-7.34, 4 x 40 7.34, 5 x 32 7.28, 3 x 64
+//    7.07, 4 x 48 6.98, 6 x 32 6.73, 8 x 16 4.94, 12 x 8 2.36;
+//  * the sustained power-capped regime (after 2,000 launches, SM clock
+//    1.5-1.6 GHz): 2 x 96 7.28-7.36, 4 x 40 7.25, 3 x 48 7.17-7.25, 2 x 80
+//    7.10-7.22, 4 x 32 6.94-7.21.
+// Copies below ~32 KiB cost ~0.5 us each per SM whatever the wait mode
+// (test_wait spin and try_wait with a suspend hint measured identical), and
+// more stages of the same size lose; 3 x 48 KiB is the best shape in the
+// regime the bench measures and within 1 % of the best sustained one.
+constexpr int kBulkStages = 3;
+constexpr int kBulkStageBytes = 49152;
 // Two-stream rings: axpy 4 stages x 2 streams x 16 KiB = 128 KiB (bigger
 // stages lose 3-4 %: its consumers also store y); dot 2 x 2 x 48 KiB.
 constexpr int kBulk2Stages = 4;

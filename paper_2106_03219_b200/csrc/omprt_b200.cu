@@ -171,6 +171,13 @@ int launch_variant(int v, const T *xp, LoopArgs la, int teams, int threads, Work
     case 39: if (bulk_ok) return launch_bulk<T, OP, 2, 114688>(xp, la, teams, threads, w, op, st); break;
     case 40: if (bulk_ok) return launch_bulk<T, OP, 3, 73728>(xp, la, teams, threads, w, op, st); break;
     case 46: if (bulk_ok) return launch_bulk<T, OP, 4, 57344>(xp, la, teams, threads, w, op, st); break;
+    // more ring shapes (profiles/r2_ring_regimes.jsonl); 37 is round 2's 2 x 96 KiB
+    case 70: if (bulk_ok) return launch_bulk<T, OP, 5, 32768>(xp, la, teams, threads, w, op, st); break;
+    case 71: if (bulk_ok) return launch_bulk<T, OP, 3, 49152>(xp, la, teams, threads, w, op, st); break;
+    case 72: if (bulk_ok) return launch_bulk<T, OP, 2, 81920>(xp, la, teams, threads, w, op, st); break;
+    case 73: if (bulk_ok) return launch_bulk<T, OP, 4, 40960>(xp, la, teams, threads, w, op, st); break;
+    case 74: if (bulk_ok) return launch_bulk<T, OP, 2, 73728>(xp, la, teams, threads, w, op, st); break;
+    case 75: if (bulk_ok) return launch_bulk<T, OP, 4, 24576>(xp, la, teams, threads, w, op, st); break;
     // interleaved CTA tiles of 64 KiB / 512 KiB / 2 MiB (every CTA streams
     // neighbouring addresses at the same time) on the default ring
     case 33: case 34: case 35:
@@ -366,7 +373,8 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
   T *op = (T *)out;
   if constexpr (std::is_same<T, double>::value && OP == OMPRT_OP_ADD) {
     if (g_variant != 0 && mode == OMPRT_MODE_SPMD &&
-        (g_variant < kOrderedLiteral || (g_variant >= 33 && g_variant <= 40) || g_variant == 46))
+        (g_variant < kOrderedLiteral || (g_variant >= 33 && g_variant <= 40) || g_variant == 46 ||
+         (g_variant >= 70 && g_variant <= 75)))
       return launch_variant<T, OP>(g_variant, xp, la, teams, threads, w, op, st);
   }
   // Integer add (mod 2^n), max and min are associative and commutative: the

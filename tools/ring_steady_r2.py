@@ -22,7 +22,7 @@ import torch  # noqa: E402
 from paper_2106_03219_b200 import runtime  # noqa: E402
 from tools.bench_configs import SEED, timeit  # noqa: E402
 
-VARIANTS = (0, 19, 37, 39, 40, 46)
+VARIANTS = tuple(int(v) for v in sys.argv[1:]) or (0, 19, 37, 39, 40, 46)
 
 
 def main():

@@ -20,7 +20,7 @@ ROOT = Path(__file__).resolve().parents[1]
 LIB = ROOT / "paper_2106_03219_b200" / "libomprt_b200.so"
 
 KERNELS = (
-    "k_reduce_bulk<double, 0, 2, 98304, false>",
+    "k_reduce_bulk<double, 0, 3, 49152, false>",
     "k_axpy_minmax_bulk<4, 16384, 4, 256>",
     "k_dot_bulk<2, 49152, 4>",
     "k_generic<long, 0, 2, false, false, 288, 7>",
