@@ -446,6 +446,16 @@ def kernel_ms(launch, reps: int, stream, G: int, dev) -> float:
     return max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / reps, G, dev)
 
 
+def parse_cpulist(text: str) -> set[int]:
+    """sysfs cpulist ("0-15,32-47\n") -> {0, ..., 15, 32, ..., 47}."""
+    cpus: set[int] = set()
+    for part in text.strip().split(","):
+        if part:
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+    return cpus
+
+
 def bind_numa(index: int) -> dict:
     """Pin this rank's host threads to the NUMA node its GPU hangs off (sysfs
     numa_node of the GPU's PCI function), so the pinned e2e buffer it
@@ -460,10 +470,7 @@ def bind_numa(index: int) -> dict:
         node = int(Path(f"/sys/bus/pci/devices/{bdf}/numa_node").read_text())
         if node < 0:
             return info
-        cpus = set()
-        for part in Path(f"/sys/devices/system/node/node{node}/cpulist").read_text().split(","):
-            a, _, b = part.strip().partition("-")
-            cpus.update(range(int(a), int(b or a) + 1))
+        cpus = parse_cpulist(Path(f"/sys/devices/system/node/node{node}/cpulist").read_text())
         cpus &= os.sched_getaffinity(0)
         if cpus:
             os.sched_setaffinity(0, cpus)
