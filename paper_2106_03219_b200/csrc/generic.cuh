@@ -212,34 +212,59 @@ constexpr uint32_t kBarFork = 1, kBarRegion = 2, kBarJoin = 3;
 constexpr int kGenericOrdDepth = 4;  // ORDERED workers: 32-byte loads in flight per lane
 
 // The team partials folded into acc strictly in team order (the fallback's
-// combine order, host.py:567-582) by one warp: the lanes load 128 partials
-// per round trip (coalesced, lane l holds b + 32k + l), then every lane walks
-// them in order through register shuffles — one dependent add per partial
-// instead of one L2 round trip per 8 (the single-thread fold_in_order was
-// ~45 us of C4's ORDERED launch at 1024 teams).  All 32 lanes call; the
-// result is the same in every lane.
-template <int OP, class T> OMPRT_D T warp_fold_in_order(T acc, const T *p, int64_t n) {
-  constexpr int K = 4;  // partials per lane per round trip (register budget of 32)
+// combine order, host.py:567-582) by one warp: the lanes stage up to `cap`
+// partials at a time into shared memory with coalesced loads (one L2 round
+// trip per block), then lane 0 adds them in order out of shared memory, the
+// loads issued eight ahead so the chain is one dependent add per partial
+// (8.2 cycles for fp64, profiles/r1_micro_latency.json).  Round 1 walked
+// them through register shuffles instead: every step waited on a shuffle,
+// ~30 cycles per partial — 16.3 us of C4's ORDERED launch at 1024 teams
+// (tools/trace_generic.py).  All 32 lanes call; the result is returned in
+// every lane.
+template <int OP, class T>
+OMPRT_D T warp_fold_in_order(T acc, const T *p, int64_t n, T *buf, int cap) {
+  constexpr int V = 16 / (int)sizeof(T);
   const uint32_t lane = lane_id();
-  for (int64_t b = 0; b < n; b += 32 * K) {
-    T v[K];
+  for (int64_t b = 0; b < n; b += cap) {
+    const int m = (int)(n - b < cap ? n - b : cap);
+    const T *src = p + b;
+    // one L2 round trip: 16-byte cp.async copies (L2 only, no registers),
+    // all of a lane's in flight at once
+    const int nv = (((uintptr_t)src & 15u) == 0) ? m / V : 0;
+    for (int i = (int)lane; i < nv; i += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(buf + (size_t)i * V)),
+                   "l"(src + (size_t)i * V)
+                   : "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    for (int i = nv * V + (int)lane; i < m; i += 32) buf[i] = ld_cg(src + i);
+    __syncwarp();
+    if (lane == 0) {
+      // the next eight are read while the current eight are added
+      int k = 0;
+      T cur[8];
+      if (m >= 8) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int64_t i = b + k * 32 + lane;
-      v[k] = i < n ? ld_cg(p + i) : Red<OP, T>::identity();
-    }
-    const int64_t m = n - b < 32 * K ? n - b : 32 * K;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-#pragma unroll
-      for (int l = 0; l < 32; ++l) {
-        const T e = __shfl_sync(0xffffffffu, v[k], l);
-        if (k * 32 + l < m) acc = Red<OP, T>::apply(acc, e);
+        for (int u = 0; u < 8; ++u) cur[u] = buf[u];
       }
+      for (; k + 8 <= m; k += 8) {
+        T nxt[8];
+        const bool more = k + 16 <= m;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) nxt[u] = more ? buf[k + 8 + u] : cur[u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = Red<OP, T>::apply(acc, cur[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+      }
+      for (; k < m; ++k) acc = Red<OP, T>::apply(acc, buf[k]);
     }
+    __syncwarp();
   }
-  return acc;
+  return __shfl_sync(0xffffffffu, acc, 0);
 }
+
+constexpr int kGenericFoldBytes = 8192;  // shared staging of the ORDERED team-partial fold
 
 // ORD: the ORDERED instance (its in-order worker loop needs more registers;
 // keeping it out of the SPMD instance keeps that one at 4 teams per SM).
@@ -324,7 +349,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
     if (last) {
       fence_acq_rel_gpu();
       if constexpr (ORD) {
-        const T v = warp_fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x);
+        __shared__ __align__(16) T s_fold[kGenericFoldBytes / sizeof(T)];
+        const T v = warp_fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x, s_fold,
+                                              (int)(kGenericFoldBytes / sizeof(T)));
         if (lane == 0 && !trap_raised()) *out = v;
       } else {
         T v = Red<OP, T>::identity();

@@ -578,6 +578,11 @@ int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, in
                       : k_generic<T, OP, 2, false, false, kGenericOneWaveThreads, 7>;
   if constexpr (std::is_floating_point<T>::value) {
     if (ordered) kern = g_trace_on ? k_generic<T, OP, 4, true, true> : k_generic<T, OP, 4, true>;
+    // teams of <= 288 threads: pinned at four teams per SM (<= 56 registers;
+    // the residency A/B in profiles/r2_c4_ordered_residency_ab.jsonl)
+    if (ordered && 32 + P <= kGenericOneWaveThreads)
+      kern = g_trace_on ? k_generic<T, OP, 4, true, true, kGenericOneWaveThreads, 4>
+                        : k_generic<T, OP, 4, true, false, kGenericOneWaveThreads, 4>;
   }
   // Physical backing of the team arena: the region's known allocation
   // footprint (pad, then parts[P+1]) capped at the semantic capacity.  The
