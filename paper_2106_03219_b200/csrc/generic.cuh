@@ -221,24 +221,29 @@ constexpr int kGenericOrdDepth = 4;  // ORDERED workers: 32-byte loads in flight
 // ~30 cycles per partial — 16.3 us of C4's ORDERED launch at 1024 teams
 // (tools/trace_generic.py).  All 32 lanes call; the result is returned in
 // every lane.
+// Stage m partials of src into shared memory with 16-byte cp.async copies
+// (L2 only, no registers; all of a lane's in flight at once, so one L2 round
+// trip), the unaligned remainder with ld.cg.  All 32 lanes call.
+template <class T> OMPRT_D void warp_stage(T *buf, const T *src, int m) {
+  constexpr int V = 16 / (int)sizeof(T);
+  const uint32_t lane = lane_id();
+  const int nv = (((uintptr_t)src & 15u) == 0) ? m / V : 0;
+  for (int i = (int)lane; i < nv; i += 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(buf + (size_t)i * V)),
+                 "l"(src + (size_t)i * V)
+                 : "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  for (int i = nv * V + (int)lane; i < m; i += 32) buf[i] = ld_cg(src + i);
+  __syncwarp();
+}
+
 template <int OP, class T>
 OMPRT_D T warp_fold_in_order(T acc, const T *p, int64_t n, T *buf, int cap) {
-  constexpr int V = 16 / (int)sizeof(T);
   const uint32_t lane = lane_id();
   for (int64_t b = 0; b < n; b += cap) {
     const int m = (int)(n - b < cap ? n - b : cap);
-    const T *src = p + b;
-    // one L2 round trip: 16-byte cp.async copies (L2 only, no registers),
-    // all of a lane's in flight at once
-    const int nv = (((uintptr_t)src & 15u) == 0) ? m / V : 0;
-    for (int i = (int)lane; i < nv; i += 32)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                       (uint32_t)__cvta_generic_to_shared(buf + (size_t)i * V)),
-                   "l"(src + (size_t)i * V)
-                   : "memory");
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    for (int i = nv * V + (int)lane; i < m; i += 32) buf[i] = ld_cg(src + i);
-    __syncwarp();
+    warp_stage(buf, p + b, m);
     if (lane == 0) {
       // the next eight are read while the current eight are added
       int k = 0;
@@ -262,6 +267,23 @@ OMPRT_D T warp_fold_in_order(T acc, const T *p, int64_t n, T *buf, int cap) {
     __syncwarp();
   }
   return __shfl_sync(0xffffffffu, acc, 0);
+}
+
+// SPMD team combine by one warp: lane l folds partials l, l+32, ... (staged
+// through shared memory, so one L2 round trip instead of one per 32), then
+// the warp tree.  cap must be a multiple of 32 (the per-lane order is that
+// of a plain strided walk over all n).
+template <int OP, class T> OMPRT_D T warp_combine(const T *p, int64_t n, T *buf, int cap) {
+  const uint32_t lane = lane_id();
+  T v = Red<OP, T>::identity();
+  for (int64_t b = 0; b < n; b += cap) {
+    const int m = (int)(n - b < cap ? n - b : cap);
+    warp_stage(buf, p + b, m);
+#pragma unroll 8
+    for (int i = (int)lane; i < m; i += 32) v = Red<OP, T>::apply(v, buf[i]);
+    __syncwarp();
+  }
+  return warp_reduce<OP, T>(v, 32);
 }
 
 constexpr int kGenericFoldBytes = 8192;  // shared staging of the ORDERED team-partial fold
@@ -354,9 +376,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
                                               (int)(kGenericFoldBytes / sizeof(T)));
         if (lane == 0 && !trap_raised()) *out = v;
       } else {
-        T v = Red<OP, T>::identity();
-        for (uint32_t i = lane; i < gridDim.x; i += 32) v = Red<OP, T>::apply(v, ld_cg(partials + i));
-        v = warp_reduce<OP, T>(v, 32);
+        __shared__ __align__(16) T s_comb[kGenericFoldBytes / sizeof(T)];
+        const T v = warp_combine<OP, T>(partials, (int64_t)gridDim.x, s_comb,
+                                        (int)(kGenericFoldBytes / sizeof(T)));
         if (lane == 0 && !trap_raised()) *out = Red<OP, T>::apply(*out, v);
       }
       if constexpr (TRACE) trace_combine();
