@@ -169,17 +169,18 @@ template <int STAGE_BYTES> struct BulkPlan {
 
 // Stream NS byte streams (same plan, different base pointers) through the
 // stage ring (stage st of stream j lives at stages + (st*NS + j)*STAGE_BYTES).
-// `consume(loc, v, r[0..NS))` is called by the consumer threads (all warps
-// but warp 0) exactly once for every 16-byte vector v of every stage; `loc`
-// (BulkPlan::Loc) locates v in the streams.
+// `stage_fn(loc, sv, nvec, ct, nc)` is called by every consumer thread (all
+// warps but warp 0; consumer index ct of nc) once per stage, with the stage's
+// vectors at sv (stream j's vector v at sv[j * STAGE_BYTES/16 + v]); `loc`
+// (BulkPlan::Loc) locates vector v in the streams.
 // The consumers release a stage with an mbarrier arrive only (the
 // producer's wait on that mbarrier orders the stage's reads before the next
 // bulk copy into it — the CUTLASS TMA-pipeline consumer_release pattern);
 // PROXY_FENCE adds a fence.proxy.async per stage (tuning variant 17).
-template <int NS, int STAGES, int STAGE_BYTES, class F, bool PROXY_FENCE = false>
-OMPRT_D void bulk_stream_n(const unsigned char *const (&base)[NS],
-                           const BulkPlan<STAGE_BYTES> &plan, unsigned char *stages,
-                           uint64_t *full, uint64_t *empty, F &&consume) {
+template <int NS, int STAGES, int STAGE_BYTES, bool PROXY_FENCE = false, class F>
+OMPRT_D void bulk_stream_stages(const unsigned char *const (&base)[NS],
+                                const BulkPlan<STAGE_BYTES> &plan, unsigned char *stages,
+                                uint64_t *full, uint64_t *empty, F &&stage_fn) {
   const uint32_t warp = warp_id(), lane = lane_id();
   const uint32_t nwarps = blockDim.x >> 5;
   const int64_t nst = plan.nstages();
@@ -213,20 +214,33 @@ OMPRT_D void bulk_stream_n(const unsigned char *const (&base)[NS],
       const int st = (int)(k % STAGES);
       mbar_wait(&full[st], (uint32_t)((k / STAGES) & 1));
       const uint32_t nvec = (uint32_t)(plan.stage_bytes(k) >> 4);
-      const typename BulkPlan<STAGE_BYTES>::Loc where = plan.loc(k);
-      const uint4 *sv = (const uint4 *)(stages + (size_t)st * NS * STAGE_BYTES);
-      for (uint32_t v = ct; v < nvec; v += nc) {
-        uint4 r[NS];
-#pragma unroll
-        for (int j = 0; j < NS; ++j) r[j] = sv[(size_t)j * (STAGE_BYTES / 16) + v];
-        consume(where, v, r);
-      }
+      stage_fn(plan.loc(k), (const uint4 *)(stages + (size_t)st * NS * STAGE_BYTES), nvec, ct,
+               nc);
       if constexpr (PROXY_FENCE)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
+}
+
+// The per-vector form: `consume(loc, v, r[0..NS))` is called by the consumer
+// threads exactly once for every 16-byte vector v of every stage.
+template <int NS, int STAGES, int STAGE_BYTES, class F, bool PROXY_FENCE = false>
+OMPRT_D void bulk_stream_n(const unsigned char *const (&base)[NS],
+                           const BulkPlan<STAGE_BYTES> &plan, unsigned char *stages,
+                           uint64_t *full, uint64_t *empty, F &&consume) {
+  bulk_stream_stages<NS, STAGES, STAGE_BYTES, PROXY_FENCE>(
+      base, plan, stages, full, empty,
+      [&](const typename BulkPlan<STAGE_BYTES>::Loc &where, const uint4 *sv, uint32_t nvec,
+          uint32_t ct, uint32_t nc) {
+        for (uint32_t v = ct; v < nvec; v += nc) {
+          uint4 r[NS];
+#pragma unroll
+          for (int j = 0; j < NS; ++j) r[j] = sv[(size_t)j * (STAGE_BYTES / 16) + v];
+          consume(where, v, r);
+        }
+      });
 }
 
 // Split the team's iteration set into a bulk plan (16-byte aligned teeth for

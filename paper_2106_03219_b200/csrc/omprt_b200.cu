@@ -18,12 +18,18 @@
 #include "generic.cuh"
 #include "ordered.cuh"
 #include "exchange.cuh"
+#include "leftext.cuh"
 
 using namespace omprt;
 
 namespace {
 
 thread_local std::string t_last_error;
+
+// Team-partial slots (8 bytes each) of the reduction-family workspace: the
+// ORDERED max/min constructs keep a (value, order key) pair per CTA for max
+// and for min (leftext.cuh).
+constexpr int kReduceSlots = 4;
 
 int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -84,6 +90,9 @@ thread_local int g_unroll = 4;   // vectors in flight per lane per iteration
 thread_local int g_variant = 0;  // kernel variant of the fp64 sum (0 = default)
 thread_local int g_spmd_block = 0;  // CUDA threads per SPMD CTA (0 = the policy below)
 constexpr int kOrderedLiteral = 20;  // variant: ORDERED mode through the literal walk
+// variant: ORDERED fp max/min through the row-group kernels (ordered.cuh)
+// instead of the leftmost-extremum SPMD kernels (leftext.cuh) — A/B and tests
+constexpr int kOrderedRowsMinMax = 76;
 bool g_trace_on = false;  // a trace ring is installed (selects traced kernel instances)
 
 int check_grid(int teams, int threads) {
@@ -234,6 +243,9 @@ void spmd_prepare(LoopArgs &la, int teams) {
 // two-stream dot from 256 (7.09-7.13 vs 6.94 at 384); axpy (read, read,
 // write) from 1024 (+1-3 % over 256-768: more warps issue the y stores).
 constexpr int kReduceBlock = 384, kAxpyBlock = 1024, kDotBlock = 256;
+// ORDERED axpy + max/min (leftext.cuh): its (value, key) trackers need more
+// registers than 1024-thread CTAs allow
+constexpr int kAxpyExtBlock = 512;
 
 int spmd_block(int threads, int pref) {
   if (g_spmd_block > 0) return g_spmd_block;
@@ -366,6 +378,25 @@ int launch_ordered_variant(int v, const T *xp, LoopArgs la, int teams, int threa
   }
 }
 
+// ORDERED fp max/min as the SPMD construct with leftmost tie-breaking
+// (leftext.cuh): order keys pack the iteration below bit 40.
+bool ext_ok(const LoopArgs &la) { return la.ub < la.lb || la.ub - la.lb < ((int64_t)1 << 40); }
+
+template <class T, int OP>
+int launch_reduce_ext(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T *op,
+                      cudaStream_t st) {
+  spmd_prepare(la, teams);
+  la.threads = threads;
+  const int blk = spmd_block(threads, kReduceBlock);
+  auto kern = blk <= kReduceBlock ? k_reduce_ext<T, OP, kBulkStages, kBulkStageBytes, kReduceBlock>
+                                  : k_reduce_ext<T, OP, kBulkStages, kBulkStageBytes>;
+  const size_t smem = BulkSmem<kBulkStages, kBulkStageBytes>::bytes;
+  int rc = set_smem(kern, smem);
+  if (rc) return rc;
+  kern<<<teams * la.split, blk, smem, st>>>(xp, la, w, op);
+  return check_launch("omprt_reduce(ordered max/min)");
+}
+
 template <class T, int OP>
 int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode, Workspace w,
                     void *out, cudaStream_t st) {
@@ -384,6 +415,10 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
   if (mode == OMPRT_MODE_ORDERED && std::is_integral<T>::value && g_variant != kOrderedLiteral)
     mode = OMPRT_MODE_SPMD;
   if (mode == OMPRT_MODE_ORDERED) {
+    if constexpr (std::is_floating_point<T>::value && OP != OMPRT_OP_ADD) {
+      if (g_variant != kOrderedLiteral && g_variant != kOrderedRowsMinMax && ext_ok(la))
+        return launch_reduce_ext<T, OP>(xp, la, teams, threads, w, op, st);
+    }
     // row-group kernels (ordered.cuh); the literal walk for small chunks,
     // pointers not 16-byte aligned, or variant kOrderedLiteral
     if constexpr (std::is_same<T, double>::value && OP == OMPRT_OP_ADD) {
@@ -815,7 +850,7 @@ int omprt_reduce_exchange(const void *d_x, int64_t lb, int64_t ub, int dtype, in
   if (threads < 64 || threads % 32 != 0)
     return fail(OMPRT_EINVAL, "reduce_exchange: threads must be a multiple of 32, >= 64");
   LoopArgs la{lb, ub, chunk, sched};
-  Workspace w = ws_carve(d_ws, teams, 2);
+  Workspace w = ws_carve(d_ws, teams, kReduceSlots);
   Exchange xc;
   xc.peers = reinterpret_cast<uint64_t *const *>(const_cast<void *>(d_peers));
   xc.rank = rank;
@@ -906,7 +941,7 @@ int omprt_bounds_dump(int64_t lb, int64_t ub, int sched, int64_t chunk, int team
 }
 
 size_t omprt_reduce_workspace_bytes(int teams, int threads, int mode) {
-  return ws_bytes(teams < 1 ? 1 : teams, threads < 1 ? 1 : threads, mode, 2);
+  return ws_bytes(teams < 1 ? 1 : teams, threads < 1 ? 1 : threads, mode, kReduceSlots);
 }
 
 int omprt_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int sched,
@@ -920,7 +955,7 @@ int omprt_reduce(const void *d_x, int64_t lb, int64_t ub, int dtype, int op, int
   if (mode != OMPRT_MODE_SPMD && mode != OMPRT_MODE_ORDERED)
     return fail(OMPRT_EINVAL, "unknown mode %d", mode);
   LoopArgs la{lb, ub, chunk, sched};
-  Workspace w = ws_carve(d_ws, teams, 2);
+  Workspace w = ws_carve(d_ws, teams, kReduceSlots);
   return by_dtype<ReduceF>(dtype, op, d_x, la, teams, threads, mode, w, d_out, S(stream));
 }
 
@@ -959,9 +994,22 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
   if (!d_ws || !d_max || !d_min || ((!d_x || !d_y) && ub >= lb))
     return fail(OMPRT_EINVAL, "axpy_minmax: null device pointer");
   LoopArgs la{lb, ub, chunk, sched};
-  Workspace w = ws_carve(d_ws, teams, 2);
+  Workspace w = ws_carve(d_ws, teams, kReduceSlots);
   if (mode != OMPRT_MODE_ORDERED)
     return launch_axpy_spmd(a, d_x, d_y, la, teams, threads, w, d_max, d_min, S(stream));
+  if (g_variant != kOrderedLiteral && g_variant != kOrderedRowsMinMax && ext_ok(la)) {
+    // one pass: the SPMD axpy with the reference order's max/min kept as the
+    // leftmost extremum (leftext.cuh) — bit-identical to the literal walk
+    spmd_prepare(la, teams);
+    la.threads = threads;
+    const int blk = spmd_block(threads, kAxpyExtBlock);
+    auto kern = blk <= kAxpyExtBlock ? k_axpy_minmax_ext<kBulk2Stages, kBulk2StageBytes, kAxpyExtBlock>
+                                     : k_axpy_minmax_ext<kBulk2Stages, kBulk2StageBytes, kMaxThreads>;
+    const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
+    if ((rc = set_smem(kern, smem))) return rc;
+    kern<<<teams * la.split, blk, smem, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+    return check_launch("omprt_axpy_minmax(ordered)");
+  }
   if (g_variant == kOrderedLiteral || !ord_rows_ok(la, d_y)) {
     k_axpy_minmax_ordered<<<teams, threads, 0, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
     return check_launch("omprt_axpy_minmax(ordered)");
@@ -1006,7 +1054,7 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
   if (!d_ws || !d_out || ((!d_x || !d_y) && ub >= lb))
     return fail(OMPRT_EINVAL, "dot: null device pointer");
   LoopArgs la{lb, ub, chunk, sched};
-  Workspace w = ws_carve(d_ws, teams, 2);
+  Workspace w = ws_carve(d_ws, teams, kReduceSlots);
   if (mode == OMPRT_MODE_ORDERED) {
     if (g_variant != kOrderedLiteral && ord_rows_ok(la, d_x, d_y)) {
       // six warps when they fill whole waves: two streams' 256-byte windows

@@ -210,3 +210,84 @@ def test_axpy_ordered_minmax_signed_zeros(cuda):
                                    mode="ordered")
     assert np.float32(gmx.item()).tobytes() == np.float32(mx).tobytes()
     assert np.float32(gmn.item()).tobytes() == np.float32(mn).tobytes()
+
+
+ROWS_MINMAX = 76  # omprt_set_variant: ORDERED fp max/min through the row-group kernels
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("op", ["max", "min"])
+def test_ordered_maxmin_leftmost_in_thread_order(cuda, dtype, op):
+    """ORDERED fp max/min run as the SPMD construct keeping the extremum with
+    the smallest position in the reference sequence (leftext.cuh).  Every
+    extremal element is a zero of random sign, so the result's sign bit is
+    decided by which zero the reference order meets first — (owner thread,
+    iteration), which for the chunked schedules is NOT iteration order
+    (chunk 1: consecutive iterations belong to consecutive threads, and the
+    owner wraps around P).  Ragged lb/ub and a misaligned base (the LDG
+    walker and scalar heads) included; the row-group kernels (variant 76)
+    must agree."""
+    dt = DTS[dtype]
+    npdt = np.float64 if dtype == "f64" else np.float32
+    n = 200_003
+    rng = np.random.default_rng(2106)
+    x = (-1.0 - rng.random(n)).astype(npdt)
+    if op == "min":
+        x = -x
+    z = rng.choice(n, 20_000, replace=False)
+    x[z] = np.where(rng.random(z.size) < 0.5, -0.0, 0.0).astype(npdt)
+    x[rng.choice(n, 500, replace=False)] = np.nan
+    ident = -np.inf if op == "max" else np.inf
+    opc = O.MAX if op == "max" else O.MIN
+    full = torch.from_numpy(x).to(cuda)
+    cases = (("static_chunked", 1, 7, 96, 0, n - 1, 0), ("static_chunked", 3, 148, 384, 5, n - 3, 0),
+             ("distribute_chunked", 1, 13, 64, 1, n - 1, 0),
+             ("distribute_chunked", 5, 148, 1024, 0, n - 2, 0), ("static", 1, 3, 100, 2, n - 1, 0),
+             ("distribute", 1, 148, 384, 0, n - 1, 0), ("static_chunked", 2, 9, 33, 0, n - 2, 1),
+             ("distribute_chunked", 7, 5, 128, 3, n - 2, 1),
+             ("static_chunked", 3, 148, 384, 5, n - 3, ROWS_MINMAX))
+    try:
+        for sched, chunk, teams, threads, lb, ub, tag in cases:
+            variant = tag if tag == ROWS_MINMAX else 0
+            off = 1 if tag == 1 else 0  # misaligned base pointer
+            xs = x[off:]
+            xd = full[off:]
+            runtime.set_variant(variant)
+            for init in (ident, 0.0, np.nan):
+                want = O.reduce(xs, lb, ub - off, dt, opc, SCHEDS[sched], chunk, teams, threads,
+                                init)
+                got = _ordered(xd, op, sched, chunk, teams, threads, lb, ub - off, init)
+                assert np.array([got]).tobytes() == np.array([want], dtype=npdt).tobytes(), \
+                    (sched, chunk, teams, threads, lb, ub, tag, init, got, want)
+    finally:
+        runtime.set_variant(0)
+
+
+@pytest.mark.gpu
+def test_axpy_ordered_leftmost_in_thread_order(cuda):
+    """C3 ORDERED in one pass (SPMD axpy + leftmost-extremum max/min): the
+    extremes are zeros of random sign, every schedule and chunk; y must equal
+    the oracle's elementwise and max/min must carry the reference order's
+    sign bits."""
+    n = 300_007
+    rng = np.random.default_rng(7)
+    x = np.where(rng.random(n) < 0.5, -0.0, 0.0).astype(np.float32)
+    y0 = np.where(rng.random(n) < 0.5, -0.0, 0.0).astype(np.float32)
+    y0[rng.choice(n, 1000, replace=False)] = np.float32(-3.0)
+    y0[rng.choice(n, 1000, replace=False)] = np.float32(3.0)
+    for sched, chunk, teams, threads in (("static_chunked", 1, 148, 384), ("static_chunked", 64, 37, 1000),
+                                          ("distribute_chunked", 1, 148, 1024),
+                                          ("distribute_chunked", 3, 11, 96), ("static", 1, 148, 384),
+                                          ("distribute", 1, 64, 256)):
+        for a in (0.75, -1.0):
+            yo = y0.copy()
+            mx, mn = O.axpy_minmax(a, x, yo, 0, n - 1, SCHEDS[sched], chunk, teams, threads,
+                                   -np.inf, np.inf)
+            yd = torch.from_numpy(y0.copy()).to(cuda)
+            gmx, gmn = runtime.axpy_minmax(a, torch.from_numpy(x).to(cuda), yd, sched=sched,
+                                           chunk=chunk, teams=teams, threads=threads,
+                                           mode="ordered")
+            assert yd.cpu().numpy().tobytes() == yo.tobytes(), (sched, chunk, a)
+            assert np.float32(gmx.item()).tobytes() == np.float32(mx).tobytes(), (sched, chunk, a)
+            assert np.float32(gmn.item()).tobytes() == np.float32(mn).tobytes(), (sched, chunk, a)
