@@ -5,7 +5,7 @@ set -x
 mkdir -p gpurun_out
 bash tools/gpu_profile.sh
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k regex:'k_axpy_minmax_bulk|k_minmax_ordered_rows|k_dot_bulk|k_generic' -s 0 -c 12 \
+  -k regex:'k_axpy_minmax_bulk|k_axpy_minmax_ext|k_reduce_ext|k_dot_bulk|k_generic' -s 0 -c 14 \
   -o gpurun_out/prof_secondary python tools/profile_kernels.py > gpurun_out/ncu_secondary.log 2>&1
 # summarise on the box (the reports themselves can exceed gpurun's 64 MiB merge)
 python tools/ncu_summary.py launches gpurun_out/launches.csv gpurun_out/launches_bench.json > /dev/null

@@ -1,7 +1,8 @@
 """Launch each secondary construct kernel twice at its BASELINE config size
 (for ncu --set full captures; see tools/gpu_r2_profile.sh): C3 SPMD flat
 static_chunked 4096 at 148x384 (balanced CTA pieces), C3 ORDERED at 148x1024
-(SPMD axpy + the reference-order max/min pass), C5 dot shard, C4 generic
+(one pass: the SPMD axpy with the leftmost-extremum max/min, leftext.cuh),
+the fp64 max ORDERED over 2^30 (same technique), C5 dot shard, C4 generic
 mode SPMD and ORDERED (fp64, 1024 teams x (32+256))."""
 import sys
 from pathlib import Path
@@ -26,6 +27,8 @@ y = runtime.synthetic(n, "f64", SEED, 1, device=dev)
 for _ in range(2):
     runtime.dot(x, y)
 del y
+for _ in range(2):
+    runtime.reduce(x, "max", sched="distribute", teams=148, threads=384, mode="ordered")
 xg = x[: 1 << 26]
 for _ in range(2):
     runtime.generic_reduce(xg, teams=1024, par_threads=256)
