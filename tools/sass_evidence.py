@@ -25,7 +25,9 @@ KERNELS = (
     "k_dot_bulk<2, 49152, 4>",
     "k_generic<long, 0, 2, false, false, 288, 7>",
     "k_generic<double, 0, 2, false, false, 288, 7>",
-    "k_generic<double, 0, 4, true, false, 1024, 1>",
+    "k_generic<double, 0, 4, true, false, 288, 4>",
+    "k_reduce_ext<double, 1, 3, 49152, 384>",
+    "k_axpy_minmax_ext<4, 16384, 512>",
     "k_reduce_ordered_rows<double, 0, 64>",
     "k_minmax_ordered_rows<128>",
     "k_dot_ordered_rows<64>",
