@@ -65,6 +65,15 @@ class DeviceGuard {
  public:
   explicit DeviceGuard(void *stream) {
     if (reinterpret_cast<uintptr_t>(stream) <= 2) return;
+    // inside a CUDA-graph capture the stream cannot be queried for its device
+    // (it would invalidate the capture): the capturing caller has its device
+    // current, so the launch is captured as is
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(S(stream), &cs) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    if (cs != cudaStreamCaptureStatusNone) return;
     int want = -1, cur = -1;
     if (cudaStreamGetDevice(S(stream), &want) != cudaSuccess) {
       cudaGetLastError();  // an invalid handle surfaces at the launch instead

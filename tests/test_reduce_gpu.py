@@ -311,3 +311,50 @@ def test_spmd_cta_size_is_unobservable(cuda):
                 and float(gmn.item()) == mn
     finally:
         runtime.set_spmd_block(0)
+
+
+@pytest.mark.gpu
+def test_constructs_capture_into_cuda_graphs(cuda):
+    """Launch-bound callers (config 1) replay the constructs from a CUDA
+    graph: every construct entry point must be capture-safe (no stream or
+    device queries that invalidate a capture) and the replays must give the
+    same results as direct launches (the ticket self-resets between them)."""
+    n = 1 << 20
+    xi = runtime.synthetic(n, "i64", O.SEED, device=cuda)
+    xf = runtime.synthetic(n, "f64", O.SEED, device=cuda)
+    ys = runtime.synthetic(n, "f32", O.SEED, 1, device=cuda)
+    xs = runtime.synthetic(n, "f32", O.SEED, device=cuda)
+    oi = torch.zeros(1, dtype=torch.int64, device=cuda)
+    od = torch.zeros(1, dtype=torch.float64, device=cuda)
+    omx = torch.full((1,), float("-inf"), dtype=torch.float32, device=cuda)
+    omn = torch.full((1,), float("inf"), dtype=torch.float32, device=cuda)
+    om = torch.full((1,), float("-inf"), dtype=torch.float64, device=cuda)
+
+    def body():
+        runtime.reduce(xi, sched="static", teams=1, threads=128, out=oi)  # config 1 (split CTAs)
+        runtime.dot(xf, xf, out=od)
+        runtime.axpy_minmax(0.0, xs, ys, sched="static_chunked", chunk=64, mode="ordered",
+                            out_max=omx, out_min=omn)
+        runtime.reduce(xf, "max", sched="distribute", mode="ordered", out=om)
+
+    s = torch.cuda.Stream(cuda)
+    s.wait_stream(torch.cuda.current_stream(cuda))
+    with torch.cuda.stream(s):
+        body()  # warm-up outside the capture (smem attributes, workspace)
+        torch.cuda.synchronize()
+        want = (oi.item(), od.item(), omx.item(), omn.item(), om.item())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            body()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        oi.zero_()
+        od.zero_()
+        omx.fill_(float("-inf"))
+        omn.fill_(float("inf"))
+        om.fill_(float("-inf"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert oi.item() == want[0]
+        assert abs(od.item() - want[1]) <= 1e-12 * abs(want[1])
+        assert (omx.item(), omn.item(), om.item()) == want[2:]
