@@ -247,9 +247,10 @@ int omprt_bounds_dump(int64_t lb, int64_t ub, int sched, int64_t chunk, int team
 /* teams distribute parallel for reduction                                    */
 /* ========================================================================= */
 
-/* Bytes of device workspace the reductions need (team partials, per-thread
- * partials for ORDERED, the last-team-finishes ticket, ORDERED's per-group
- * ready flags).  The workspace must be zeroed once before first use; the
+/* Bytes of device workspace the reductions need (team partials — for
+ * ORDERED max/min a (value, order key) pair per team for max and for min —,
+ * per-thread partials for ORDERED, the last-team-finishes ticket, ORDERED's
+ * per-group ready flags).  The workspace must be zeroed once before first use; the
  * ticket self-resets (atomic inc wraps, devicert.step_inc
  * devicert.py:105-107) and the ready flags carry a fresh 64-bit key per
  * launch, so it can be reused across launches (of any kernel) on one

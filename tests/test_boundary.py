@@ -99,14 +99,15 @@ def test_allreduce_argument_checks():
 
 def test_workspace_layout_covers_split_teams_and_ordered_flags():
     # SPMD launches may split a few teams over up to SMs CTAs: the team
-    # partial slots (2 per CTA, 8 bytes) never shrink below 256 CTAs; ORDERED
+    # partial slots (4 per CTA, 8 bytes: ORDERED max/min keep a (value, order
+    # key) pair for max and for min) never shrink below 256 CTAs; ORDERED
     # keeps P partials plus one 8-byte ready flag per group of 32 threads
     L = _lib.load()
     for teams, threads in ((1, 128), (3, 64), (148, 256), (1024, 1024), (7, 33)):
         spmd = L.omprt_reduce_workspace_bytes(teams, threads, 0)
         ordered = L.omprt_reduce_workspace_bytes(teams, threads, 1)
         P = teams * threads
-        assert spmd >= 256 + max(teams, 256) * 8 * 2
+        assert spmd >= 256 + max(teams, 256) * 8 * 4
         assert ordered >= spmd + P * 8 + ((P + 31) // 32) * 8
 
 
