@@ -288,6 +288,23 @@ template <int OP, class T> OMPRT_D T warp_combine(const T *p, int64_t n, T *buf,
 
 constexpr int kGenericFoldBytes = 8192;  // shared staging of the ORDERED team-partial fold
 
+// ORDERED generic mode: the team that draws this ticket becomes the folder
+// of the team partials (in team order, as they are published), from about
+// half-way through the launch; below 256 teams the last team folds them all
+// (UINT32_MAX: no folder).
+OMPRT_HD uint32_t gen_fold_ticket(uint32_t teams) {
+  return teams >= 256 ? teams / 2 : 0xffffffffu;
+}
+
+OMPRT_D void st_release_gpu_u64(uint64_t *p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+OMPRT_D uint64_t ld_acquire_gpu_u64(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ORD: the ORDERED instance (its in-order worker loop needs more registers;
 // keeping it out of the SPMD instance keeps that one at 4 teams per SM).
 // TRACE: the instance with the trace-ring hooks, launched only while a ring
@@ -301,7 +318,7 @@ template <class T, int OP, int U, bool ORD = false, bool TRACE = false, int MAXT
           int MINB = 1>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_generic(const T *__restrict__ x, int64_t lb, int64_t ub, int P, int ordered, int64_t pad,
-              ArenaCfg cfg, Workspace ws, T *out, int64_t *team_offsets) {
+              ArenaCfg cfg, Workspace ws, T *out, int64_t *team_offsets, uint64_t epoch) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ ArenaState st;
   __shared__ volatile int s_work;
@@ -356,32 +373,84 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
     // -------------------------------------- teams reduction within the main warps
     T *partials = (T *)ws.team_partials;
-    int last = 0;
-    if (lane == 0) {
-      partials[blockIdx.x] = team_val;
-      fence_acq_rel_gpu();
-      const uint32_t t = atomic_inc_acq_rel_gpu(ws.ticket, gridDim.x - 1);
-      last = t == gridDim.x - 1;
-      if constexpr (TRACE) {
-        trace_record(blockIdx.x, kTraceTeam, t, trace_t0());
-        if (last) trace_t0() = globaltimer();
+    if constexpr (ORD) {
+      // ORDERED: the team partials are folded strictly in team order.  Most
+      // of that chain need not wait for the last team: the team that draws
+      // ticket teams/2 stays on as the folder and folds the partials as they
+      // are published (ready flags carry the launch's epoch), overlapping
+      // the chain with the teams still streaming.
+      uint64_t *flags = (uint64_t *)(ws.team_partials + (size_t)partial_slots(gridDim.x) * 8);
+      uint32_t t = 0;
+      if (lane == 0) {
+        partials[blockIdx.x] = team_val;
+        st_release_gpu_u64(flags + blockIdx.x, epoch);
+        fence_acq_rel_gpu();
+        t = atomic_inc_acq_rel_gpu(ws.ticket, gridDim.x - 1);
+        if constexpr (TRACE) {
+          trace_record(blockIdx.x, kTraceTeam, t, trace_t0());
+          if (t == gridDim.x - 1) trace_t0() = globaltimer();
+        }
       }
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-      fence_acq_rel_gpu();
-      if constexpr (ORD) {
-        __shared__ __align__(16) T s_fold[kGenericFoldBytes / sizeof(T)];
-        const T v = warp_fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x, s_fold,
-                                              (int)(kGenericFoldBytes / sizeof(T)));
+      t = __shfl_sync(0xffffffffu, t, 0);
+      __shared__ __align__(16) T s_fold[kGenericFoldBytes / sizeof(T)];
+      constexpr int cap = (int)(kGenericFoldBytes / sizeof(T));
+      const uint32_t tfold = gen_fold_ticket(gridDim.x);
+      if (t == tfold) {
+        // the folder: extends the folded prefix as the teams publish, so at
+        // the end only the last few partials remain
+        if constexpr (TRACE) {
+          if (lane == 0) trace_t0() = globaltimer();
+        }
+        T acc = *out;
+        int64_t K = 0;
+        while (K < (int64_t)gridDim.x) {
+          int64_t R = K;  // the ready frontier, 32 flags a step, at most one staging block
+          for (;;) {
+            const int64_t i = R + lane;
+            const bool ready = i < (int64_t)gridDim.x && ld_acquire_gpu_u64(flags + i) == epoch;
+            const uint32_t m = __ballot_sync(0xffffffffu, ready);
+            const int k = m == 0xffffffffu ? 32 : __ffs(~m) - 1;
+            R += k;
+            if (k < 32 || R - K >= cap) break;
+          }
+          if (R == K) {
+            __nanosleep(256);
+            continue;
+          }
+          fence_acq_rel_gpu();  // every lane's acquire before any lane's partial loads
+          acc = warp_fold_in_order<OP, T>(acc, partials + K, R - K, s_fold, cap);
+          K = R;
+        }
+        if (lane == 0 && !trap_raised()) *out = acc;
+        if constexpr (TRACE) trace_combine();
+      } else if (tfold >= gridDim.x && t == gridDim.x - 1) {
+        // few teams: the last one folds them all
+        fence_acq_rel_gpu();
+        const T v = warp_fold_in_order<OP, T>(*out, partials, (int64_t)gridDim.x, s_fold, cap);
         if (lane == 0 && !trap_raised()) *out = v;
-      } else {
+        if constexpr (TRACE) trace_combine();
+      }
+    } else {
+      int last = 0;
+      if (lane == 0) {
+        partials[blockIdx.x] = team_val;
+        fence_acq_rel_gpu();
+        const uint32_t t = atomic_inc_acq_rel_gpu(ws.ticket, gridDim.x - 1);
+        last = t == gridDim.x - 1;
+        if constexpr (TRACE) {
+          trace_record(blockIdx.x, kTraceTeam, t, trace_t0());
+          if (last) trace_t0() = globaltimer();
+        }
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        fence_acq_rel_gpu();
         __shared__ __align__(16) T s_comb[kGenericFoldBytes / sizeof(T)];
         const T v = warp_combine<OP, T>(partials, (int64_t)gridDim.x, s_comb,
                                         (int)(kGenericFoldBytes / sizeof(T)));
         if (lane == 0 && !trap_raised()) *out = Red<OP, T>::apply(*out, v);
+        if constexpr (TRACE) trace_combine();
       }
-      if constexpr (TRACE) trace_combine();
     }
   } else {
     // ------------------------------------------------ worker state machine

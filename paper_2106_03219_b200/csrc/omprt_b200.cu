@@ -645,7 +645,8 @@ int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, in
     if (e != cudaSuccess)
       return fail(OMPRT_ECUDA, "generic: smem attribute: %s", cudaGetErrorString(e));
   }
-  kern<<<teams, 32 + P, smem, st>>>((const T *)x, lb, ub, P, ordered, pad, cfg, w, (T *)out, offs);
+  kern<<<teams, 32 + P, smem, st>>>((const T *)x, lb, ub, P, ordered, pad, cfg, w, (T *)out, offs,
+                                    next_epoch());
   return check_launch("omprt_generic_reduce");
 }
 
@@ -667,7 +668,8 @@ int launch_generic_op(int op, const void *x, int64_t lb, int64_t ub, int teams, 
   return fail(OMPRT_EINVAL, "unknown reduction op %d", op);
 }
 
-size_t generic_ws_core(int teams) { return ws_bytes(teams, 0, OMPRT_MODE_SPMD, 1); }
+// team partials + (ORDERED) one epoch-tagged ready flag per team
+size_t generic_ws_core(int teams) { return ws_bytes(teams, 0, OMPRT_MODE_SPMD, 2); }
 
 // Host-buffer (tgt_target-shaped) entries: device staging cached per CUDA
 // device (a buffer belongs to the context it was allocated in, so a caller

@@ -75,6 +75,8 @@ runtime.set_spmd_block(0)
 runtime.axpy_minmax(0.5, xf, yf, sched="distribute", teams=148, threads=1024, mode="ordered")
 runtime.generic_reduce(x, teams=64, par_threads=256)
 runtime.generic_reduce(x, teams=64, par_threads=256, ordered=True)
+# >= 256 teams: the ORDERED folder team folds the partials as they are published
+runtime.generic_reduce(x, teams=300, par_threads=64, ordered=True)
 runtime.bounds_dump(0, 99_999, "static_chunked", 3, teams=4, threads=64, device=dev)
 runtime.generic_reduce(xi, teams=16, par_threads=64)
 runtime.generic_reduce(xi, teams=16, par_threads=64, ordered=True)
