@@ -287,3 +287,27 @@ def test_generic_config4_size(cuda):
         else:
             exact = O.exact_sum_gen(0, n - 1, O.F64, k=4)
             assert abs(float(out.item()) - exact) <= 1e-6 * exact
+
+
+@pytest.mark.gpu
+def test_generic_ordered_folder_team(cuda):
+    """ORDERED generic mode with >= 256 teams: the team drawing ticket
+    teams/2 folds the team partials in team order as they are published.
+    Bit-identical to the reference order at ragged sizes; a trapping launch
+    (arena overflow in every team) leaves the cell unwritten; back-to-back
+    launches reuse the workspace (epoch-tagged flags, no re-zeroing)."""
+    for teams, P, n in ((256, 64, 1_000_003), (300, 32, 777_777), (1024, 96, 1 << 20)):
+        x = runtime.synthetic(n, "f64", O.SEED, 5, device=cuda)
+        want = O.generic_reduce(None, 0, n - 1, O.F64, O.ADD, teams, P, 0.0, seed=O.SEED, k=5)
+        for _ in range(3):
+            out = torch.zeros(1, dtype=torch.float64, device=cuda)
+            runtime.generic_reduce(x, teams=teams, par_threads=P, ordered=True, out=out)
+            assert runtime.check_trap(cuda) is None
+            assert out.cpu().numpy().tobytes() == np.array([want]).tobytes(), (teams, P, n)
+    x = runtime.synthetic(1 << 16, "f64", O.SEED, 9, device=cuda)
+    out = torch.full((1,), 7.0, dtype=torch.float64, device=cuda)
+    runtime.generic_reduce(x, teams=300, par_threads=64, ordered=True, pad_bytes=65536 - 256,
+                           out=out)
+    trap = runtime.check_trap(cuda)
+    assert trap is not None and trap.kind == 1
+    assert out.item() == 7.0  # on a trap the folder does not write the cell
