@@ -65,7 +65,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--ordered-steps", type=int, default=50,
                    help="steps of the ORDERED-mode (reference-order, bit-identical) leg")
-    p.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU (weak leg)")
+    p.add_argument("--n-per-gpu", "--n", dest="n", type=int, default=N_PER_GPU,
+                   help="elements per GPU (weak leg)")
     p.add_argument("--strong-n", type=int, default=1 << 30,
                    help="global elements of the strong-scaled C2 leg")
     p.add_argument("--c5-n", type=int, default=1 << 33,
@@ -97,9 +98,13 @@ def spawn_ranks(args) -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
+    # torch.distributed.run's parser would take an abbreviation of its own
+    # options out of the script's arguments ("--n" matches "--nnodes", ...)
+    argv = ["--n-per-gpu" + a[3:] if a == "--n" or a.startswith("--n=") else a
+            for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+           "--master-port", str(port), str(ROOT / "bench.py"), *argv]
     print(f"bench: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
     return subprocess.call(cmd)
 

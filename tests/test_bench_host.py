@@ -64,3 +64,27 @@ def test_defaults_are_the_headline_config(monkeypatch):
 def test_committed_capture_is_of_the_bench_kernel():
     d = json.loads((ROOT / "profiles" / "ncu_bench_kernel.json").read_text())
     assert bench.BENCH_KERNEL in d["launches"][0]["kernel"]
+
+
+def test_spawned_argv_survives_torchrun_parsing(monkeypatch):
+    """--gpus N > 1 re-launches under torch.distributed.run; none of the
+    script's options may be taken as an abbreviation of torchrun's own
+    (`--n` would match --nnodes / --nproc-per-node)."""
+    import subprocess
+
+    from torch.distributed import run as trun
+
+    captured = {}
+    monkeypatch.setattr(subprocess, "call", lambda cmd: captured.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "8", "--n", "1024", "--steps", "3",
+                                      "--warmup", "3", "--backend", "gloo", "--no-legs",
+                                      "--teams", "4", "--threads", "64", "--exchange", "p2p"])
+    bench.spawn_ranks(bench.parse())
+    cmd = captured["cmd"]
+    i = cmd.index("torch.distributed.run")
+    ns = trun.get_args_parser().parse_args(cmd[i + 1:])
+    assert ns.nproc_per_node == "8" and ns.training_script.endswith("bench.py")
+    monkeypatch.setattr(sys, "argv", ["bench.py", *ns.training_script_args])
+    a = bench.parse()
+    assert (a.gpus, a.n, a.steps, a.backend, a.teams, a.threads, a.exchange) == \
+        (8, 1024, 3, "gloo", 4, 64, "p2p")
