@@ -207,3 +207,58 @@ def test_reduce_exchange_single_rank_matches_reduce(cuda):
         assert runtime.check_trap(cuda) is None
     finally:
         L.omprt_mailbox_destroy(mb)
+
+
+def _nccl_worker(port: int, q) -> None:
+    """One rank over a real NCCL process group: the bench's overlapped
+    step (ShardedStep: the shard construct on the compute stream, the
+    8-byte NCCL all-reduce + combine on a side stream, double-buffered
+    partials), the integer all-reduce through parallel.reduce_sharded, a
+    device-side barrier and the max-over-ranks timing reduction."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    from paper_2106_03219_b200 import parallel, runtime
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        n = 1 << 22
+        x = runtime.synthetic(n, "i64", O.SEED, 3, device=dev)
+        out = torch.zeros(1, dtype=torch.int64, device=dev)
+        stream = torch.cuda.current_stream(dev)
+        step = bench.ShardedStep(lambda p: runtime.reduce(x, "add", out=p), out, 2, stream,
+                                 overlap=True)  # G = 2: take the collective path with 1 rank
+        for _ in range(5):
+            step.step()
+        step.drain()
+        torch.cuda.synchronize()
+        res = {"overlapped_5_steps": int(out.item())}
+        o2 = torch.zeros(1, dtype=torch.int64, device=dev)
+        parallel.reduce_sharded(x, "add", out=o2, deterministic=False)
+        res["allreduce"] = int(o2.item())
+        dist.barrier()
+        res["max_over_ranks"] = bench.max_over_ranks(1.5, 2, dev)
+        q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_process_group_one_rank_overlapped_step(cuda):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    want = int(O.reduce(None, 0, (1 << 22) - 1, O.I64, O.ADD, O.STATIC, 1, 1, 1, k=3))
+    wrap = lambda v: (v + (1 << 63)) % (1 << 64) - (1 << 63)  # noqa: E731
+    assert res["overlapped_5_steps"] == wrap(5 * want)
+    assert res["allreduce"] == want
+    assert res["max_over_ranks"] == 1.5
