@@ -38,6 +38,18 @@ def main():
     N = 6_000_011
     data = {dt: O.fill(N, dt, O.SEED, 5) for dt in (O.F32, O.F64, O.I64, O.U32)}
     dev_data = {dt: torch.from_numpy(v).to(dev) for dt, v in data.items()}
+    # zero-heavy data for the ORDERED max/min tie rule: every extremal element
+    # is a zero of random sign (plus NaNs), so the result's sign bit is decided
+    # by the reference sequence's order (owner thread, iteration)
+    zr = np.random.default_rng(a.seed + 1)
+    zdata = {}
+    for dt, npdt in ((O.F32, np.float32), (O.F64, np.float64)):
+        z = (-1.0 - zr.random(N)).astype(npdt)
+        idx = zr.choice(N, N // 8, replace=False)
+        z[idx] = np.where(zr.random(idx.size) < 0.5, -0.0, 0.0).astype(npdt)
+        z[zr.choice(N, 1000, replace=False)] = np.nan
+        zdata[dt] = z
+    zdev = {dt: torch.from_numpy(v).to(dev) for dt, v in zdata.items()}
     y64 = O.fill(N, O.F64, O.SEED, 6)
     y64d = torch.from_numpy(y64).to(dev)
     fails, kinds = [], {}
@@ -49,7 +61,8 @@ def main():
         lb = int(rng.integers(0, 100))
         ub = int(rng.integers(lb - 2, N))
         kind = str(rng.choice(["sum64", "sum32", "max64", "min32", "dot", "axpy",
-                               "spmd_i64", "spmd_u32max", "spmd_f64", "spmd_dot", "spmd_axpy"]))
+                               "spmd_i64", "spmd_u32max", "spmd_f64", "spmd_dot", "spmd_axpy",
+                               "zmax64", "zmax32", "zmin64", "zmin32"]))
         kinds[kind] = kinds.get(kind, 0) + 1
         # SPMD kinds also draw the CTA size (omprt_set_spmd_block; 0 = policy)
         blk = int(rng.choice([0, 0, 0, 64, 96, 256, 384, 1024])) if kind.startswith("spmd") else 0
@@ -99,6 +112,21 @@ def main():
                            threads=threads, mode="ordered", out=out)
             got = out.cpu().numpy()[0]
             ok = np.array([got]).tobytes() == np.array([want], dtype=data[dt].dtype).tobytes()
+        elif kind.startswith("z"):
+            # ORDERED max/min on zero-heavy data (min: negated, the extreme is
+            # again a zero); the cell starts at the identity, 0.0 or NaN
+            dt = O.F64 if kind.endswith("64") else O.F32
+            op = kind[1:4]
+            xs = zdata[dt] if op == "max" else -zdata[dt]
+            xd = zdev[dt] if op == "max" else -zdev[dt]
+            init = float(rng.choice([-np.inf if op == "max" else np.inf, 0.0, np.nan]))
+            want = O.reduce(xs, lb, ub, dt, O.MAX if op == "max" else O.MIN, SCHEDS[sched],
+                            chunk, teams, threads, init)
+            out = torch.full((1,), init, dtype=xd.dtype, device=dev)
+            runtime.reduce(xd, op, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
+                           threads=threads, mode="ordered", out=out)
+            got = out.cpu().numpy()[0]
+            ok = np.array([got]).tobytes() == np.array([want], dtype=xs.dtype).tobytes()
         elif kind == "dot":
             want = O.dot(data[O.F64], y64, lb, ub, SCHEDS[sched], chunk, teams, threads)
             got = float(runtime.dot(dev_data[O.F64], y64d, lb=lb, ub=ub, sched=sched, chunk=chunk,
