@@ -51,6 +51,15 @@ SEED = 0x210603219
 BENCH_KERNEL = "k_reduce_bulk<double, 0, 3, 49152, 0>"
 
 
+def workload_config(n: int, G: int, sched: str, teams: int, threads: int) -> dict:
+    """The `config` both arms print (identical dicts, so the driver can match
+    them): the C2 workload at G GPUs, n elements per GPU."""
+    return {"workload": "C2 teams distribute parallel for fp64 sum reduction, SPMD",
+            "n_per_gpu": n, "n_global": G * n, "schedule": sched, "teams": teams,
+            "threads": threads, "mode": "spmd", "parallelism": f"dp{G}",
+            "l2": "input 8 GiB per GPU >> 126 MB L2; no flush needed"}
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -335,12 +344,12 @@ def run_reference_arm(args) -> None:
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (splitmix64 counter-based fp64 in [0,1), in host memory)",
-        "config": {"workload": "C2 teams distribute parallel for fp64 sum reduction, SPMD",
-                   "n_per_gpu": n, "n_global": n, "schedule": "distribute",
-                   "teams": teams, "threads": args.threads},
+        "config": workload_config(n, args.gpus, args.sched, teams, args.threads),
         "cpu_baseline": {"value": round(r["gbs"], 3), "unit": "GB/s", "cores": r["cores"],
                          "kind": "port",
-                         "sample": f"the full workload: {n} fp64 elements ({n * 8 >> 20} MiB) "
+                         "sample": (f"the full workload: {n}" if args.gpus == 1 else
+                                    f"one GPU's share of the {args.gpus}-GPU workload: {n}") +
+                                   f" fp64 elements ({n * 8 >> 20} MiB) "
                                    f"per step, host fallback order (host.py:567-582) over "
                                    f"{teams}x{args.threads} OpenMP threads, parallel over "
                                    "host cores"},
@@ -706,19 +715,14 @@ def run_ours(args) -> None:
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (splitmix64 counter-based fp64 in [0,1), generated on device)",
-            "config": {"workload": "C2 teams distribute parallel for fp64 sum reduction, SPMD",
-                       "n_per_gpu": n, "n_global": G * n, "schedule": args.sched,
-                       "teams": teams, "threads": threads, "mode": "spmd",
-                       "parallelism": (f"dp{G} (static_bounds shards + partials exchanged inside "
-                                       "the reduction kernel over NVLink peer memory)"
-                                       if px is not None else
-                                       f"dp{G} (static_bounds shards + {args.backend.upper()} "
-                                       "all-reduce" + (", overlapped with the next step's shard)"
-                                                       if (G > 1 and not args.no_overlap)
-                                                       else ")")),
-                       "l2": "input 8 GiB per GPU >> 126 MB L2; no flush needed",
-                       "frac_of_hbm_peak": round(gbs / G / pk["hbm_gbs"], 4),
-                       "frac_of_nominal_8tbs": round(gbs / G / 8000.0, 4)},
+            "config": workload_config(n, G, args.sched, teams, threads),
+            "combine": (f"static_bounds shards + partials exchanged inside the reduction kernel "
+                        "over NVLink peer memory" if px is not None else
+                        f"static_bounds shards + {args.backend.upper()} all-reduce" +
+                        (", overlapped with the next step's shard"
+                         if (G > 1 and not args.no_overlap) else "")) if G > 1 else "none (one GPU)",
+            "frac_of_hbm_peak": round(gbs / G / pk["hbm_gbs"], 4),
+            "frac_of_nominal_8tbs": round(gbs / G / 8000.0, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2),
                          "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / pk["hbm_gbs"], 4),

@@ -88,3 +88,17 @@ def test_spawned_argv_survives_torchrun_parsing(monkeypatch):
     a = bench.parse()
     assert (a.gpus, a.n, a.steps, a.backend, a.teams, a.threads, a.exchange) == \
         (8, 1024, 3, "gloo", 4, 64, "p2p")
+
+
+def test_both_arms_print_the_same_config():
+    """The reference arm and ours describe the workload with the same dict
+    (the driver matches them); measured values stay out of `config`."""
+    import inspect
+
+    c1 = bench.workload_config(1 << 30, 1, "distribute", 148, 384)
+    c8 = bench.workload_config(1 << 30, 8, "distribute", 148, 384)
+    assert c1["n_global"] == 1 << 30 and c8["n_global"] == 8 << 30 and c8["parallelism"] == "dp8"
+    assert not any(isinstance(v, float) for v in c1.values())
+    src_ref = inspect.getsource(bench.run_reference_arm)
+    src_ours = inspect.getsource(bench.run_ours)
+    assert '"config": workload_config(' in src_ref and '"config": workload_config(' in src_ours
