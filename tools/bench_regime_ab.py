@@ -30,7 +30,8 @@ x = runtime.synthetic(n, "f64", 0x210603219, 0, device=dev)
 out = torch.zeros(1, dtype=torch.float64, device=dev)
 s = torch.cuda.current_stream(dev)
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 6
-variants = [int(v) for v in sys.argv[2:]] or [0, 12, 19, 36, 46]
+# "bN" entries: the default kernel on N-thread CTAs (omprt_set_spmd_block)
+variants = [v if v.startswith("b") else int(v) for v in sys.argv[2:]] or [0, 12, 19, 36, 46]
 
 
 def step():
@@ -63,11 +64,15 @@ res: dict[int, list[float]] = {v: [] for v in variants}
 for r in range(rounds):
     order = variants[r % len(variants):] + variants[:r % len(variants)]
     for v in order:
-        runtime.set_variant(v)
+        if isinstance(v, str):
+            runtime.set_spmd_block(int(v[1:]))
+        else:
+            runtime.set_variant(v)
         try:
             ms = block()
         finally:
             runtime.set_variant(0)
+            runtime.set_spmd_block(0)
         res[v].append(round(n * 8 / ms / 1e6, 1))
         time.sleep(1.0)
 for v in variants:
