@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const uint32_t nall = 32u + (uint32_t)P;
   const uint32_t lane = lane_id();
   if constexpr (TRACE) trace_begin();
+  else pdl_begin();
 
   if (warp_id() == 0) {
     // ------------------------------------------------ main warp (sequential part)

@@ -412,7 +412,19 @@ OMPRT_D uint64_t &trace_t0() {
   return t0;
 }
 // thread 0, at the top of a construct kernel
+// Programmatic dependent launch: a construct launched with the PDL launch
+// attribute may start while the previous kernel of its stream drains; it
+// waits for that kernel's completion (and memory) before touching global
+// memory, and lets its own dependents launch at once (they wait the same
+// way, and only launch once every CTA of this grid has started).  Both are
+// no-ops for a kernel launched without the attribute.
+OMPRT_D void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 OMPRT_D void trace_begin() {
+  pdl_begin();
   if (threadIdx.x == 0 && g_trace.recs) trace_t0() = globaltimer();
 }
 // thread 0: record slot `slot` (CTA index, or gridDim.x + k for extras)

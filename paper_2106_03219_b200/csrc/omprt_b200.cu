@@ -13,6 +13,7 @@
 #include <string>
 #include <type_traits>
 #include <unordered_map>
+#include <utility>
 
 #include "bulk.cuh"
 #include "generic.cuh"
@@ -104,6 +105,29 @@ constexpr int kOrderedLiteral = 20;  // variant: ORDERED mode through the litera
 constexpr int kOrderedRowsMinMax = 76;
 bool g_trace_on = false;  // a trace ring is installed (selects traced kernel instances)
 
+// Construct kernels are launched with programmatic dependent launch (PDL):
+// the next construct on a stream gets its CTAs resident while the previous
+// one drains, then waits in pdl_begin() (omprt.cuh) for its completion —
+// the launch gap of back-to-back constructs is hidden.  Variant kNoPdl
+// launches them plainly (A/B).
+constexpr int kNoPdl = 77;
+
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_variant == kNoPdl ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 int check_grid(int teams, int threads) {
   if (teams < 1) return fail(OMPRT_EINVAL, "teams must be >= 1 (got %d)", teams);
   if (threads < 1 || threads > kMaxThreads)
@@ -154,7 +178,7 @@ int launch_bulk(const T *xp, LoopArgs la, int teams, int threads, Workspace w, T
   const size_t smem = BulkSmem<STAGES, SB>::bytes;
   int rc = set_smem(kern, smem);
   if (rc) return rc;
-  kern<<<teams * (la.split > 1 ? la.split : 1), threads, smem, st>>>(xp, la, w, op);
+  launch_k(kern, teams * (la.split > 1 ? la.split : 1), threads, smem, st, xp, la, w, op);
   return check_launch("omprt_reduce(bulk)");
 }
 
@@ -402,7 +426,7 @@ int launch_reduce_ext(const T *xp, LoopArgs la, int teams, int threads, Workspac
   const size_t smem = BulkSmem<kBulkStages, kBulkStageBytes>::bytes;
   int rc = set_smem(kern, smem);
   if (rc) return rc;
-  kern<<<teams * la.split, blk, smem, st>>>(xp, la, w, op);
+  launch_k(kern, teams * la.split, blk, smem, st, xp, la, w, op);
   return check_launch("omprt_reduce(ordered max/min)");
 }
 
@@ -520,8 +544,8 @@ int launch_exchange_t(const void *x, LoopArgs la, int teams, int threads, Worksp
   if (rc) return rc;
   spmd_prepare(la, teams);
   la.threads = threads;
-  kern<<<teams * la.split, spmd_block(threads, kReduceBlock), smem, st>>>((const T *)x, la, w,
-                                                                          (T *)out, xc);
+  launch_k(kern, teams * la.split, spmd_block(threads, kReduceBlock), smem, st, (const T *)x, la,
+           w, (T *)out, xc);
   return check_launch("omprt_reduce_exchange");
 }
 
@@ -645,8 +669,8 @@ int launch_generic_t(const void *x, int64_t lb, int64_t ub, int teams, int P, in
     if (e != cudaSuccess)
       return fail(OMPRT_ECUDA, "generic: smem attribute: %s", cudaGetErrorString(e));
   }
-  kern<<<teams, 32 + P, smem, st>>>((const T *)x, lb, ub, P, ordered, pad, cfg, w, (T *)out, offs,
-                                    next_epoch());
+  launch_k(kern, teams, 32 + P, smem, st, (const T *)x, lb, ub, P, ordered, pad, cfg, w, (T *)out,
+           offs, next_epoch());
   return check_launch("omprt_generic_reduce");
 }
 
@@ -982,13 +1006,13 @@ int launch_axpy_spmd(float a, const float *d_x, float *d_y, LoopArgs la, int tea
     auto kern = g_variant == 47 ? k_axpy_minmax_bulk<2, 49152, 4> : k_axpy_minmax_bulk<3, 32768, 4>;
     const size_t smem = g_variant == 47 ? (size_t)2 * 2 * 49152 : (size_t)2 * 3 * 32768;
     if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams * la.split, blk, smem, st>>>(a, d_x, d_y, la, w, d_max, d_min);
+    launch_k(kern, teams * la.split, blk, smem, st, a, d_x, d_y, la, w, d_max, d_min);
   } else if (g_unroll == 4) {
     auto kern = blk <= 256 ? k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4, 256>
                            : k_axpy_minmax_bulk<kBulk2Stages, kBulk2StageBytes, 4>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
     if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams * la.split, blk, smem, st>>>(a, d_x, d_y, la, w, d_max, d_min);
+    launch_k(kern, teams * la.split, blk, smem, st, a, d_x, d_y, la, w, d_max, d_min);
   } else {
     k_axpy_minmax<4><<<teams * la.split, blk, 0, st>>>(a, d_x, d_y, la, w, d_max, d_min);
   }
@@ -1018,7 +1042,7 @@ int omprt_axpy_minmax(float a, const float *d_x, float *d_y, int64_t lb, int64_t
                                      : k_axpy_minmax_ext<kBulk2Stages, kBulk2StageBytes, kMaxThreads>;
     const size_t smem = (size_t)2 * kBulk2Stages * kBulk2StageBytes;
     if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<teams * la.split, blk, smem, S(stream)>>>(a, d_x, d_y, la, w, d_max, d_min);
+    launch_k(kern, teams * la.split, blk, smem, S(stream), a, d_x, d_y, la, w, d_max, d_min);
     return check_launch("omprt_axpy_minmax(ordered)");
   }
   if (g_variant == kOrderedLiteral || !ord_rows_ok(la, d_y)) {
@@ -1113,14 +1137,14 @@ int omprt_dot(const double *d_x, const double *d_y, int64_t lb, int64_t ub, int 
       auto kern = k_dot_bulk<3, 32768, 4>;
       const size_t smem = (size_t)2 * 3 * 32768;
       if ((rc = set_smem(kern, smem))) return rc;
-      kern<<<teams * la.split, blk, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
+      launch_k(kern, teams * la.split, blk, smem, S(stream), d_x, d_y, la, w, d_out);
     } else if (g_unroll == 4) {
       // 2 stages x 2 streams x 48 KiB (7.50 vs 7.42 TB/s for 4 x 2 x 16 KiB,
       // steady state, profiles/r2_ring2_steady.jsonl)
       auto kern = k_dot_bulk<kDotStages, kDotStageBytes, 4>;
       const size_t smem = (size_t)2 * kDotStages * kDotStageBytes;
       if ((rc = set_smem(kern, smem))) return rc;
-      kern<<<teams * la.split, blk, smem, S(stream)>>>(d_x, d_y, la, w, d_out);
+      launch_k(kern, teams * la.split, blk, smem, S(stream), d_x, d_y, la, w, d_out);
     } else if (g_unroll >= 8) {
       k_dot<8><<<teams * la.split, blk, 0, S(stream)>>>(d_x, d_y, la, w, d_out);
     } else {
