@@ -129,6 +129,8 @@ def lib_path() -> Path:
 def load(build_if_missing: bool = False):
     """Load (and bind) the shared library; never falls back to Python."""
     global _lib
+    if _lib is not None:  # bound once; the lock only guards the first load
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib

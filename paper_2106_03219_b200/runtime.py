@@ -65,8 +65,10 @@ def stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _stream(t: torch.Tensor) -> C.c_void_p:
-    return C.c_void_p(stream_handle(t.device))
+def _stream(t: torch.Tensor) -> int:
+    # a plain int: the bound argtypes (c_void_p) convert it, and building a
+    # c_void_p per argument is a measurable part of a small launch's host time
+    return stream_handle(t.device)
 
 
 def _dev(t: torch.Tensor) -> torch.device:
@@ -88,8 +90,8 @@ def _check_range(lb: int, ub: int, *bufs: tuple[str, torch.Tensor]) -> None:
             raise IndexError(f"iteration space [{lb}, {ub}] escapes {name}[0:{t.numel()}]")
 
 
-def _p(t: torch.Tensor | None) -> C.c_void_p:
-    return C.c_void_p(0 if t is None else t.data_ptr())
+def _p(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
 
 
 _sms: dict[int, int] = {}
@@ -325,9 +327,10 @@ def reduce(x: torch.Tensor, op="add", *, lb: int = 0, ub: int | None = None, sch
     if ub is None:
         ub = lb + x.numel() - 1
     _check_range(lb, ub, ("x", x))
-    g = default_grid(dev)
-    teams = teams or g.teams
-    threads = threads or g.threads
+    if not (teams and threads):
+        g = default_grid(dev)
+        teams = teams or g.teams
+        threads = threads or g.threads
     if out is None:
         out = torch.zeros(1, dtype=x.dtype, device=dev)
         if init is not None:
