@@ -111,6 +111,11 @@ bool g_trace_on = false;  // a trace ring is installed (selects traced kernel in
 // the launch gap of back-to-back constructs is hidden.  Variant kNoPdl
 // launches them plainly (A/B).
 constexpr int kNoPdl = 77;
+// SPMD reductions whose pieces are under this many bytes per CTA take the
+// LDG walker instead of the TMA ring (default variant only: any tuning
+// variant, e.g. kNoSmallPath, keeps the ring — the ring tests use that)
+constexpr int64_t kSmallPieceBytes = 96 * 1024;
+constexpr int kNoSmallPath = 78;
 
 template <class... KArgs, class... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -479,13 +484,18 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
     la.threads = threads;
     const int grid = teams * la.split;
     const int blk = spmd_block(threads, kReduceBlock);
-    if (g_unroll == 4) {
+    // Small pieces per CTA (config 1: 8 MiB over 148 CTAs) are latency-bound:
+    // the ring would wait for a whole first stage to land; eight 16-byte
+    // loads in flight per lane cover the piece in about one round trip.
+    const int64_t n = la.ub - la.lb + 1;
+    const bool small = n > 0 && n * (int64_t)sizeof(T) < (int64_t)grid * kSmallPieceBytes;
+    if (g_unroll == 4 && !(small && g_variant == 0)) {
       // default SPMD path: TMA bulk-copy stage ring
       return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, blk, w, op, st);
-    } else if (g_unroll >= 8) {
-      k_reduce<T, OP, 8><<<grid, blk, 0, st>>>(xp, la, w, op);
+    } else if (g_unroll >= 8 || (small && g_variant == 0)) {
+      launch_k(k_reduce<T, OP, 8>, grid, blk, 0, st, xp, la, w, op);
     } else {
-      k_reduce<T, OP, 2><<<grid, blk, 0, st>>>(xp, la, w, op);
+      launch_k(k_reduce<T, OP, 2>, grid, blk, 0, st, xp, la, w, op);
     }
   }
   return check_launch("omprt_reduce");

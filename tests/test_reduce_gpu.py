@@ -205,16 +205,22 @@ def test_full_size_int64_and_fp64(cuda):
 def test_bulk_ring_stress(cuda):
     # many short rings: partial last stages, one-stage teams, teams with no
     # vector part, every stage count; the result must be exact every time
+    # (variant 78 keeps small pieces on the ring instead of the LDG walker)
     x = runtime.synthetic(3_000_017, "i64", O.SEED, 11, device=cuda)
     xn = x.cpu().numpy()
-    for lb, ub, teams, threads in ((0, 3_000_016, 148, 256), (7, 2_999_999, 1000, 64),
-                                   (1, 40_000, 3, 96), (0, 4096 * 4 - 1, 4, 128)):
-        want = int(O.reduce(xn, lb, ub, O.I64, O.ADD, O.STATIC, 1, 1, 1))
-        out = torch.zeros(1, dtype=torch.int64, device=cuda)
-        for _ in range(200):
-            runtime.reduce(x, lb=lb, ub=ub, sched="distribute", teams=teams, threads=threads,
-                           out=out)
-        assert int(out.item()) == (want * 200 + 2**63) % 2**64 - 2**63
+    try:
+        for variant in (0, 78):
+            runtime.set_variant(variant)
+            for lb, ub, teams, threads in ((0, 3_000_016, 148, 256), (7, 2_999_999, 1000, 64),
+                                           (1, 40_000, 3, 96), (0, 4096 * 4 - 1, 4, 128)):
+                want = int(O.reduce(xn, lb, ub, O.I64, O.ADD, O.STATIC, 1, 1, 1))
+                out = torch.zeros(1, dtype=torch.int64, device=cuda)
+                for _ in range(200):
+                    runtime.reduce(x, lb=lb, ub=ub, sched="distribute", teams=teams,
+                                   threads=threads, out=out)
+                assert int(out.item()) == (want * 200 + 2**63) % 2**64 - 2**63, (variant, lb, ub)
+    finally:
+        runtime.set_variant(0)
 
 
 @pytest.mark.parametrize("dtype", ["f64", "i32", "u64"])
