@@ -409,8 +409,11 @@ __global__ void __launch_bounds__(kMaxThreads)
   const T team_val = block_reduce<OP, T>(body.total(), scratch, blockDim.x);
   T *partials = (T *)ws.team_partials;
   if (teams_ticket<OP, T>(team_val, partials, ws.ticket)) {
+    // the cell's old value loaded alongside the partials (one round trip
+    // less on the combine's critical path; nothing else writes it meanwhile)
+    const T cell = threadIdx.x == 0 ? *out : Red<OP, T>::identity();
     const T v = combine_team_partials<OP, T>(partials, scratch);
-    if (threadIdx.x == 0) *out = Red<OP, T>::apply(*out, v);
+    if (threadIdx.x == 0) *out = Red<OP, T>::apply(cell, v);
     trace_combine();
   }
 }
