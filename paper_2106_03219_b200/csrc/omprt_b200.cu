@@ -492,7 +492,11 @@ int launch_reduce_t(const void *x, LoopArgs la, int teams, int threads, int mode
     if (g_unroll == 4 && !(small && g_variant == 0)) {
       // default SPMD path: TMA bulk-copy stage ring
       return launch_bulk<T, OP, kBulkStages, kBulkStageBytes>(xp, la, teams, blk, w, op, st);
-    } else if (g_unroll >= 8 || (small && g_variant == 0)) {
+    } else if (small && g_variant == 0 && g_unroll == 4) {
+      // up to 96 KiB per CTA: 16 vectors in flight per lane of a 384-thread
+      // CTA cover the piece in one round trip
+      launch_k(k_reduce<T, OP, 16>, grid, blk, 0, st, xp, la, w, op);
+    } else if (g_unroll >= 8) {
       launch_k(k_reduce<T, OP, 8>, grid, blk, 0, st, xp, la, w, op);
     } else {
       launch_k(k_reduce<T, OP, 2>, grid, blk, 0, st, xp, la, w, op);
