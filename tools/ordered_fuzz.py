@@ -32,6 +32,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=400)
     ap.add_argument("--seed", type=int, default=2106)
+    ap.add_argument("--variant", type=int, default=0,
+                    help="omprt_set_variant for the ORDERED sum kinds (row-kernel A/B)")
+    ap.add_argument("--kinds", default="", help="comma-separated subset of kinds")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     dev = torch.device("cuda", 0)
@@ -60,7 +63,8 @@ def main():
         threads = int(rng.choice([32, 64, 96, 128, 256, 1024, int(rng.integers(1, 1025))]))
         lb = int(rng.integers(0, 100))
         ub = int(rng.integers(lb - 2, N))
-        kind = str(rng.choice(["sum64", "sum32", "max64", "min32", "dot", "axpy",
+        kind = str(rng.choice(a.kinds.split(",") if a.kinds else
+                              ["sum64", "sum32", "max64", "min32", "dot", "axpy",
                                "spmd_i64", "spmd_u32max", "spmd_f64", "spmd_dot", "spmd_axpy",
                                "zmax64", "zmax32", "zmin64", "zmin32"]))
         kinds[kind] = kinds.get(kind, 0) + 1
@@ -108,8 +112,12 @@ def main():
             want = O.reduce(data[dt], lb, ub, dt, {"add": O.ADD, "max": O.MAX, "min": O.MIN}[op],
                             SCHEDS[sched], chunk, teams, threads, init)
             out = torch.full((1,), init, dtype=dev_data[dt].dtype, device=dev)
-            runtime.reduce(dev_data[dt], op, lb=lb, ub=ub, sched=sched, chunk=chunk, teams=teams,
-                           threads=threads, mode="ordered", out=out)
+            runtime.set_variant(a.variant if op == "add" else 0)
+            try:
+                runtime.reduce(dev_data[dt], op, lb=lb, ub=ub, sched=sched, chunk=chunk,
+                               teams=teams, threads=threads, mode="ordered", out=out)
+            finally:
+                runtime.set_variant(0)
             got = out.cpu().numpy()[0]
             ok = np.array([got]).tobytes() == np.array([want], dtype=data[dt].dtype).tobytes()
         elif kind.startswith("z"):
