@@ -364,3 +364,44 @@ def test_constructs_capture_into_cuda_graphs(cuda):
         assert oi.item() == want[0]
         assert abs(od.item() - want[1]) <= 1e-12 * abs(want[1])
         assert (omx.item(), omn.item(), om.item()) == want[2:]
+
+
+@pytest.mark.gpu
+def test_concurrent_host_threads_and_streams(cuda):
+    """A multi-threaded host program: four threads, each on its own stream
+    (own cached workspace), launch constructs concurrently — tuning knobs are
+    per thread, the ticket of each workspace self-resets — and every result
+    is exact."""
+    import threading
+
+    n = 1 << 21
+    xi = runtime.synthetic(n, "i64", O.SEED, 21, device=cuda)
+    want = int(O.reduce(None, 0, n - 1, O.I64, O.ADD, O.STATIC, 1, 1, 1, k=21))
+    errors = []
+
+    def work(tid: int) -> None:
+        try:
+            s = torch.cuda.Stream(cuda)
+            with torch.cuda.stream(s):
+                runtime.set_spmd_block([0, 256, 512, 96][tid])  # per-thread knob
+                out = torch.zeros(1, dtype=torch.int64, device=cuda)
+                for _ in range(50):
+                    runtime.reduce(xi, sched=["static", "distribute", "static_chunked",
+                                              "distribute_chunked"][tid], chunk=64,
+                                   teams=[148, 37, 1, 300][tid], threads=[384, 256, 128, 64][tid],
+                                   out=out)
+                s.synchronize()
+                got = int(out.item())
+                runtime.set_spmd_block(0)
+            exp = (want * 50 + 2**63) % 2**64 - 2**63
+            if got != exp:
+                errors.append((tid, got, exp))
+        except Exception as e:  # noqa: BLE001
+            errors.append((tid, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
