@@ -141,7 +141,7 @@ DEFAULT_THREADS = int(os.environ.get("OMPRT_DEFAULT_THREADS", "384"))
 def default_grid(device: torch.device | None = None, threads: int | None = None,
                  teams_per_sm: int = 1) -> Grid:
     """A persistent grid: teams_per_sm resident teams on every SM (one team
-    per SM holds the 128 KiB bulk-copy ring; 384 threads = 1 producer + 11
+    per SM holds the 3 x 48 KiB bulk-copy ring; 384 threads = 1 producer + 11
     consumer warps, which keep the ring drained when the power cap lowers
     the SM clock — profiles/r1_threads_sweep_256_384.txt)."""
     if device is not None:
