@@ -139,20 +139,27 @@ RT_D void rt_count(u64 n) {
 }
 
 // Seeded interleaving (the vgpu's sched_seed, vgpu.py:285-306): with a
-// nonzero seed every thread sleeps a splitmix64-drawn 0..2047 ns before each
-// atomic and barrier, keyed by (seed, team, thread, instructions executed so
-// far), so a seed perturbs which thread reaches a racing operation first and
-// different seeds explore different orders.  The hardware still decides the
-// final order, so a seed does not replay a schedule bit for bit; seed 0 keeps
-// the hardware's own interleaving.
+// nonzero seed every thread sleeps before each atomic and barrier for a
+// splitmix64-drawn time keyed by (seed, team, warp, instructions executed so
+// far) — 0..4095 ns, the same for the whole warp, so warps really do arrive
+// in different orders (a per-lane draw made every warp wait for its slowest
+// lane, ~2 us, and two warps then raced as without a seed) — plus a per-lane
+// 0..255 ns.  A seed perturbs which thread reaches a racing operation first
+// and different seeds explore different orders; the hardware still decides
+// the final order, so a seed does not replay a schedule bit for bit; seed 0
+// keeps the hardware's own interleaving.
+RT_D u64 rt_mix(u64 z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
 RT_D void rt_jitter(u64 k) {
   const u64 seed = rt_ctx.seed;
   if (seed == 0) return;
-  u64 z = seed ^ ((u64)blockIdx.x << 40) ^ ((u64)threadIdx.x << 20) ^ (k * 0x9e3779b97f4a7c15ull);
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  z ^= z >> 31;
-  __nanosleep((u32)(z & 2047u));
+  const u64 base = seed ^ ((u64)blockIdx.x << 40) ^ (k * 0x9e3779b97f4a7c15ull);
+  const u64 zw = rt_mix(base ^ ((u64)(threadIdx.x >> 5) << 24));
+  const u64 zl = rt_mix(base ^ ((u64)threadIdx.x << 20) ^ 0x5bd1e995ull);
+  __nanosleep((u32)(zw & 4095u) + (u32)(zl & 255u));
 }
 
 RT_D u64 rt_label(const P &p) { return ((u64)p.space << 32) | p.label; }

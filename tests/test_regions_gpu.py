@@ -303,7 +303,9 @@ def test_sched_seed_explores_interleavings(bridge):
     # one chain 0 -> g1+1 -> ... through all 64 threads, ending in cell[0].
     B.FAST_PATH = False
     finals = set()
-    for seed in range(1, 9):
+    for seed in range(1, 17):
+        if len(finals) >= 2 and seed > 4:
+            break
         got = run_source(RACE, device="b200", sched_seed=seed)
         assert got.exit_status == 0 and all(s == 0 for _, s in got.offloads)
         vals = [int(v) for v in got.stdout.split()]
