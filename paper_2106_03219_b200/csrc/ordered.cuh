@@ -31,6 +31,7 @@
 // the stream.
 #pragma once
 
+#include "exactfold.cuh"
 #include "kernels.cuh"
 
 namespace omprt {
@@ -554,6 +555,11 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
 #pragma unroll
   for (int k = 0; k < N; ++k) ring[lane * N + k] = L.v[k];
   if (nb > 1) ord_folder_load<T>(tp, P, flags, epoch, 1, L);
+  // fp sums: a batch whose chain stays inside one binade folds 32 lanes wide
+  // (exactfold.cuh, same bits); after a miss (a binade crossing, a tie, a
+  // zero / non-finite value) the next attempts back off, so data that never
+  // qualifies pays at most one attempt per 16 batches
+  int wait = 0, miss = 0;
   for (int64_t b = 0; b < nb; ++b) {
     T *cur = ring + (b & 1) * kFoldPer;
     T *nxt = ring + ((b + 1) & 1) * kFoldPer;
@@ -564,6 +570,21 @@ OMPRT_D T ord_folder(const T *tp, int64_t P, const uint64_t *flags, uint64_t epo
     if (b + 2 < nb) ord_folder_load<T>(tp, P, flags, epoch, b + 2, L);
     __syncwarp();
     const int64_t base = b * kFoldPer;
+    if constexpr (std::is_floating_point<T>::value) {
+      T mine[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) mine[k] = cur[lane * N + k];  // zero past P
+      if (wait > 0) {
+        --wait;
+      } else if (exact_fold_batch<T, N>(acc, mine)) {
+        miss = 0;
+        __syncwarp();
+        continue;
+      } else {
+        miss = miss < 4 ? miss + 1 : 4;
+        wait = (1 << miss) - 1;
+      }
+    }
     if (base + kFoldPer <= P) {
 #pragma unroll 32
       for (int j = 0; j < kFoldPer; ++j) acc = comb(acc, cur[j]);

@@ -21,6 +21,9 @@ for teams, threads in ((148, 256), (148, 384), (148, 1024), (296, 512)):
     t0 = int(r["t_begin"][r["t_begin"] > 0].min())
     end = (st["t_end"].astype(np.int64) - t0) / 1e3
     print(json.dumps({"teams": teams, "threads": threads, "partials": teams * threads,
+                      "streams_p10_us": round(float(np.percentile(end, 10)), 1),
                       "streams_p50_us": round(float(np.median(end)), 1),
+                      "streams_p90_us": round(float(np.percentile(end, 90)), 1),
+                      "stream_records": int(len(st)),
                       "streams_last_us": round(float(end.max()), 1),
                       "folder_done_us": round((int(fo["t_end"]) - t0) / 1e3, 1)}), flush=True)
