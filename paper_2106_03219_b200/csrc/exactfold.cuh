@@ -97,4 +97,40 @@ OMPRT_D bool exact_fold_batch(T &acc, const T (&v)[N]) {
   return true;
 }
 
+// acc (lane 0's value on entry; the same in every lane on return) folded with
+// p[0..m) in order, 256 partials a step through exact_fold_batch, lane 0's
+// one-add-at-a-time chain for a step that does not qualify (after a miss the
+// next attempts back off: at most one per 16 steps on data that never
+// qualifies).  p is read in place (shared or global).  All 32 lanes of a
+// full warp call.
+template <class T> OMPRT_D T warp_sum_in_order(T acc, const T *p, int m) {
+  constexpr int N = 8;
+  const uint32_t lane = threadIdx.x & 31u;
+  acc = __shfl_sync(0xffffffffu, acc, 0);
+  int wait = 0, miss = 0;
+  for (int k0 = 0; k0 < m; k0 += 32 * N) {
+    const int mm = m - k0 < 32 * N ? m - k0 : 32 * N;
+    if (wait == 0) {
+      T mine[N];
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        const int i = (int)lane * N + u;
+        mine[u] = i < mm ? p[k0 + i] : T(0);
+      }
+      if (exact_fold_batch<T, N>(acc, mine)) {
+        miss = 0;
+        continue;
+      }
+      miss = miss < 4 ? miss + 1 : 4;
+      wait = (1 << miss) - 1;
+    } else {
+      --wait;
+    }
+    if (lane == 0)
+      for (int k = 0; k < mm; ++k) acc = acc + p[k0 + k];
+    acc = __shfl_sync(0xffffffffu, acc, 0);
+  }
+  return acc;
+}
+
 }  // namespace omprt

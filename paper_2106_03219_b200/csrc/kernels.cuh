@@ -12,6 +12,7 @@
 //   k_combine           ordered combine of per-rank partials
 #pragma once
 
+#include "exactfold.cuh"
 #include "loops.cuh"
 
 namespace omprt {
@@ -407,6 +408,15 @@ OMPRT_D T fold_in_order_team(T acc, const T *p, int64_t n, T *buf, int cap) {
         for (uint32_t w = 0; w < (blockDim.x + 31u) / 32u; ++w) acc = Red<OP, T>::apply(acc, buf[w]);
       __syncthreads();
       continue;
+    }
+    if constexpr (std::is_floating_point<T>::value) {
+      // fp sums: warp 0 folds the staged block 32 lanes wide where the chain
+      // stays inside one binade (exactfold.cuh, the same bits)
+      if (blockDim.x >= 32) {
+        if (threadIdx.x < 32) acc = warp_sum_in_order<T>(acc, buf, m);
+        __syncthreads();
+        continue;
+      }
     }
     if (threadIdx.x == 0) {
       int k = 0;

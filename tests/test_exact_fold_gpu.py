@@ -23,15 +23,20 @@ pytestmark = pytest.mark.gpu
 GEOMS = [(148, 384), (7, 33), (3, 1000)]
 
 
+SCHED = {"static": O.STATIC, "distribute": O.DISTRIBUTE, "static_chunked": O.STATIC_CHUNKED}
+
+
 def _check(cuda, x: np.ndarray, init: float, teams: int, threads: int, sched="static"):
+    """sched static / distribute: the row-group kernels and their folder warp;
+    static_chunked (chunk 1, below the row kernels' minimum chunk): the literal
+    walk, whose last team folds the thread partials (fold_in_order_team)."""
     dt = O.F64 if x.dtype == np.float64 else O.F32
     n = x.size
-    want = O.reduce(x, 0, n - 1, dt, O.ADD, {"static": O.STATIC, "distribute": O.DISTRIBUTE}[sched],
-                    1, teams, threads, init)
+    want = O.reduce(x, 0, n - 1, dt, O.ADD, SCHED[sched], 1, teams, threads, init)
     xd = torch.from_numpy(x).to(cuda)
     out = torch.full((1,), init, dtype=xd.dtype, device=cuda)
-    runtime.reduce(xd, "add", sched=sched, teams=teams, threads=threads, mode="ordered",
-                   out=out)
+    runtime.reduce(xd, "add", sched=sched, chunk=1, teams=teams, threads=threads,
+                   mode="ordered", out=out)
     got = out.cpu().numpy()[0]
     w = np.array([want], dtype=x.dtype)
     if np.isnan(w[0]):
@@ -86,7 +91,8 @@ def test_crafted_chains(cuda, ftype):
         big = np.full(P, np.finfo(ftype).max / 4)
         cases.append((big, 0.0))  # overflows to +inf in the chain
         for x, init in cases:
-            _check(cuda, np.ascontiguousarray(x, dtype=ftype), init, teams, threads)
+            for sched in ("static", "static_chunked"):
+                _check(cuda, np.ascontiguousarray(x, dtype=ftype), init, teams, threads, sched)
 
 
 @pytest.mark.parametrize("ftype", [np.float64, np.float32])
@@ -106,7 +112,7 @@ def test_random_exponent_chains(cuda, ftype):
         k = rng.random(n) < 0.05
         e = np.frexp(abs(init))[1] - 1 - mant
         x[k] = (2 * rng.integers(0, 8, int(k.sum())) + 1) * 2.0 ** (e - 1)
-        sched = "static" if trial % 2 == 0 else "distribute"
+        sched = ("static", "distribute", "static_chunked")[(trial // 3) % 3]
         _check(cuda, np.ascontiguousarray(x, dtype=ftype), init, teams, threads, sched)
 
 

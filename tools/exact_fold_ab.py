@@ -50,6 +50,24 @@ for teams, threads in ((148, 256), (148, 384), (148, 1024)):
                       "gbs": round(N * 8 / ms / 1e6, 1),
                       "bit_identical": float(out.item()) == want}), flush=True)
 
+# the literal walk (chunk 1 is below the row kernels' minimum): its last team
+# folds the P thread partials (fold_in_order_team)
+for teams, threads in ((148, 384),):
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def lstep():
+        out.zero_()
+        runtime.reduce(x, "add", sched="static_chunked", chunk=1, teams=teams, threads=threads,
+                       mode="ordered", out=out)
+
+    ms = timed(lstep, reps=5)
+    want = float(O.reduce(None, 0, N - 1, O.F64, O.ADD, O.STATIC_CHUNKED, 1, teams, threads,
+                          0.0, seed=S))
+    print(json.dumps({"lib": tag, "what": "f64 sum ORDERED 2^30 literal walk (static_chunked 1)",
+                      "teams": teams, "threads": threads, "ms": round(ms, 4),
+                      "gbs": round(N * 8 / ms / 1e6, 1),
+                      "bit_identical": float(out.item()) == want}), flush=True)
+
 del x
 n = 1 << 28
 xd = runtime.synthetic(n, "f64", S, 0, device=dev)
