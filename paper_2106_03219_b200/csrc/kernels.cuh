@@ -463,6 +463,46 @@ OMPRT_D T fold_row_in_order(const T *__restrict__ x, int64_t lo, int64_t hi, T p
   return part;
 }
 
+// The thread's iterations in order (block schedules: [lower, upper]; chunked:
+// `chunk`-long runs from lower by stride up to limit), with D loads issued
+// ahead of the in-order fold: only the fold is a dependent chain, the
+// addresses are known, so each lane keeps D loads in flight instead of one
+// round trip per element (small chunks otherwise walk at one element per
+// L2/HBM latency: 0.63 TB/s for a chunk-1 ORDERED sum at 148 x 384).
+template <int D, class V, class LoadF, class FoldF>
+OMPRT_D void walk_in_order_ahead(const Bounds &bd, bool chunked, int64_t chunk, LoadF &&load,
+                                 FoldF &&fold) {
+  const int64_t limit = chunked ? bd.limit : bd.upper;
+  int64_t lo = bd.lower;
+  if (lo > limit) return;
+  int64_t hi = chunked && lo + chunk - 1 < limit ? lo + chunk - 1 : limit;
+  int64_t i = lo;
+  bool live = true;
+  while (live) {
+    V v[D];
+    int cnt = 0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (live) {
+        v[d] = load(i);
+        ++cnt;
+        if (++i > hi) {
+          lo += bd.stride;
+          if (!chunked || lo > limit) {
+            live = false;
+          } else {
+            i = lo;
+            hi = lo + chunk - 1 < limit ? lo + chunk - 1 : limit;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (d < cnt) fold(v[d]);
+  }
+}
+
 // This thread's schedule chunks as [lo, hi] runs, in order (block schedules:
 // one run; chunked: run_thread_chunks' sequence, loops.cuh).
 template <class F> OMPRT_D void for_each_thread_run(const LoopArgs &la, F &&f) {
@@ -521,6 +561,11 @@ __global__ void __launch_bounds__(kMaxThreads)
                                     threadIdx.x, blockDim.x);
     if (la.sched != OMPRT_SCHED_STATIC_CHUNKED && la.sched != OMPRT_SCHED_DISTRIBUTE_CHUNKED) {
       part = fold_row_in_order<OP, T>(x, bd.lower, bd.upper, part);
+    } else if (la.chunk < 16) {
+      // small chunks: element loads issued ahead of the fold
+      walk_in_order_ahead<8, T>(
+          bd, true, la.chunk, [&](int64_t i) { return __ldg(x + i); },
+          [&](T v) { part = Red<OP, T>::apply(part, v); });
     } else {
       for (int64_t lo = bd.lower; lo <= bd.limit; lo += bd.stride) {
         int64_t hi = lo + la.chunk - 1;
@@ -564,8 +609,15 @@ __global__ void __launch_bounds__(kMaxThreads)
                   Workspace ws, double *out) {
   trace_begin();
   double part = 0.0;
-  run_thread_chunks(la.sched, la.lb, la.ub, la.chunk,
-                    [&](int64_t i) { part = __fma_rn(x[i], y[i], part); });
+  {
+    const Bounds bd = schedule_init(la.sched, la.lb, la.ub, la.chunk, blockIdx.x, gridDim.x,
+                                    threadIdx.x, blockDim.x);
+    const bool chunked =
+        la.sched == OMPRT_SCHED_STATIC_CHUNKED || la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED;
+    walk_in_order_ahead<6, double2>(
+        bd, chunked, la.chunk, [&](int64_t i) { return make_double2(__ldg(x + i), __ldg(y + i)); },
+        [&](double2 v) { part = __fma_rn(v.x, v.y, part); });
+  }
   __shared__ double buf[kFoldBuf];
   double *tp = (double *)ws.thread_partials;
   tp[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = part;

@@ -1,5 +1,7 @@
-"""ORDERED fp sums / dot with the folder's exact 32-lane batch fold vs without
-(A/B of two library builds: run once per library with OMPRT_B200_LIB set).
+"""ORDERED fp sums / dot with the folder's exact 32-lane batch fold vs without,
+and the literal walk (chunk < 16) with loads issued ahead of the fold vs one
+round trip per element (A/B of two library builds: run once per library with
+OMPRT_B200_LIB set).
 Every result is checked bit-for-bit against the oracle's reference order.
 
     OMPRT_B200_LIB=... python tools/exact_fold_ab.py <tag>"""
@@ -83,6 +85,18 @@ for teams, threads in ((148, 384), (148, 1024)):
     ms = timed(dstep)
     print(json.dumps({"lib": tag, "what": "f64 dot ORDERED 2^28", "teams": teams,
                       "threads": threads, "ms": round(ms, 4),
+                      "gbs": round(n * 16 / ms / 1e6, 1)}), flush=True)
+for teams, threads in ((148, 384),):
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def ldstep():
+        out.zero_()
+        runtime.dot(xd, yd, sched="static_chunked", chunk=1, teams=teams, threads=threads,
+                    mode="ordered", out=out)
+
+    ms = timed(ldstep, reps=5)
+    print(json.dumps({"lib": tag, "what": "f64 dot ORDERED 2^28 literal walk (static_chunked 1)",
+                      "teams": teams, "threads": threads, "ms": round(ms, 4),
                       "gbs": round(n * 16 / ms / 1e6, 1)}), flush=True)
 del xd, yd
 xf = runtime.synthetic(1 << 30, "f32", S, device=dev)
