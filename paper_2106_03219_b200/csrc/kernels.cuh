@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       part = fold_row_in_order<OP, T>(x, bd.lower, bd.upper, part);
     } else if (la.chunk < 16) {
       // small chunks: element loads issued ahead of the fold
-      walk_in_order_ahead<8, T>(
+      walk_in_order_ahead<16, T>(
           bd, true, la.chunk, [&](int64_t i) { return __ldg(x + i); },
           [&](T v) { part = Red<OP, T>::apply(part, v); });
     } else {
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kMaxThreads)
                                     threadIdx.x, blockDim.x);
     const bool chunked =
         la.sched == OMPRT_SCHED_STATIC_CHUNKED || la.sched == OMPRT_SCHED_DISTRIBUTE_CHUNKED;
-    walk_in_order_ahead<6, double2>(
+    walk_in_order_ahead<8, double2>(
         bd, chunked, la.chunk, [&](int64_t i) { return make_double2(__ldg(x + i), __ldg(y + i)); },
         [&](double2 v) { part = __fma_rn(v.x, v.y, part); });
   }
