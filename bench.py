@@ -603,7 +603,7 @@ def run_ours(args) -> None:
         ordered = {"value": round(nloc * ELEM / (o_ms / 1e3) / 1e9, 3), "unit": "GB/s",
                    "ms_per_step": round(o_ms, 5), "steps": args.ordered_steps,
                    "kernel": "omprt::k_reduce_ordered_rows (row-group cp.async windows + "
-                             "folder warp)",
+                             "folder warp, exact 32-lane batch fold of the partials)",
                    "result": got_ordered}
 
     # end to end through the C-ABI host-buffer call (pinned host -> HBM each
